@@ -1,0 +1,161 @@
+/* lbgpu — B200 (sm_100a) engine for the LBM primal / discrete-adjoint hot
+ * path of the reference (arxiv/paper_1501_04741, /root/reference/proj).
+ *
+ * This is the thin C ABI the GPU path sits behind (seam "B2").
+ * Each entry point replaces one operator of the reference's inner seam; the
+ * reference interface it replaces is cited beside it. Plain pointers and
+ * sizes only; all host arrays use the reference's layout: SoA planes of the
+ * current (pre-collision) state, plane p at p*N, node index
+ * x + nx*(y + ny*z) (lattice.hpp:25-27, :54-100).
+ *
+ * Status codes are the reference's (lbopt.h:18-25). Errors store a message
+ * on the engine (lbgpu_error_message), cleared on success (capi.cpp:39-59);
+ * creation failures go to thread-local storage (lbgpu_last_create_error).
+ * An engine is not thread-safe; use one per host thread. Every call is
+ * synchronous on return.
+ */
+#ifndef LBGPU_H
+#define LBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  LBGPU_OK = 0,        /* LBOPT_OK */
+  LBGPU_E_ARG = 1,     /* LBOPT_E_ARG: null handle or bad argument */
+  LBGPU_E_CONFIG = 2,  /* LBOPT_E_CONFIG: invalid system description */
+  LBGPU_E_NUMERIC = 3, /* LBOPT_E_NUMERIC: rho <= 0, non-finite residual, CUDA fault */
+  LBGPU_E_IO = 4,      /* LBOPT_E_IO */
+  LBGPU_E_STATE = 5    /* LBOPT_E_STATE: operation out of order */
+};
+
+typedef struct lbgpu_engine lbgpu_engine; /* opaque; owns all device memory */
+
+/* Flattened lbopt::System + ObjectiveSpec (collision.hpp:74-88,
+ * objective.hpp:19-28). The caller keeps ownership of every array; the
+ * engine copies what it needs. The lattice pair is implied by nz:
+ * nz == 1 -> D2Q9 flow + D2Q9 temperature, else D3Q19 + D3Q7
+ * (config.cpp:404-410). */
+typedef struct {
+  int nx, ny, nz;
+  int precision;  /* 64 | 32 ([model] precision, config.hpp:26) */
+  int exact;      /* 1: reference operation order, no FMA (FP64 only): bit-exact */
+  int device;     /* CUDA device ordinal */
+  /* ModelSpec (collision.hpp:46-59) */
+  int collision;  /* 0 fmrt, 1 bgk */
+  double nu, beta_fluid, beta_solid, inlet_dp, u_clamp, omega_nonhydro, switch_theta;
+  int switch_form; /* 0 solid_power, 1 fluid_power */
+  /* Optional: ModelTables::A (mf x mf, row-major) and the relaxation
+   * diagonal (mf). NULL -> built here the way ModelTables::build does. */
+  const double* A;
+  const double* relax;
+  /* Optional: coupled velocity table (m x 3) and opposite map (m) of
+   * System::finalize; when given they must match the engine's bit-exactly. */
+  const int32_t* vel;
+  const int32_t* opp;
+  /* TagMap + DesignField, N entries each (collision.hpp:25-41, topology.hpp:15-27) */
+  const uint8_t* tag; /* NodeTag: 0 interior 1 wall 2 inlet 3 outlet 4 heater */
+  const double* bc_T;
+  const int8_t* bc_axis;
+  const int8_t* bc_sign;
+  const double* w;
+  const uint8_t* design_mask;
+  /* ObjectiveSpec */
+  int obj_kind; /* 0 mixing 1 heatflux 2 synthetic */
+  int flux_axis, flux_sign;
+  const int64_t* support; /* ascending flat indices */
+  int64_t n_support;
+} lbgpu_system_desc;
+
+/* One monitoring row (run_record.hpp:11-19): iteration, residual,
+ * objective, penalty, penalty_weight, composite, grad_norm. */
+typedef struct {
+  double iteration, residual, objective, penalty, penalty_weight, composite, grad_norm;
+} lbgpu_run_row;
+
+const char* lbgpu_version(void);
+
+/* --- lifecycle --- */
+int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out);
+/* Build the System from case-file text (CaseConfig::parse_text + newline-
+ * separated "section.key=value" overrides + build_case, config.cpp:129-427)
+ * and create the engine. exact as in lbgpu_system_desc. */
+int lbgpu_create_from_config(const char* cfg_text, const char* overrides, int device, int exact,
+                             lbgpu_engine** out);
+void lbgpu_destroy(lbgpu_engine* e);
+/* Host-only: the System build_case would assemble from this case text, in
+ * reference form (tags, bc arrays, design w/mask/nodes, support, A), without
+ * touching a GPU. dims/counts as lbgpu_info; any array pointer may be NULL. */
+int lbgpu_case_tables(const char* cfg_text, const char* overrides, int* dims, int64_t* counts,
+                      uint8_t* tag, double* bc_T, int8_t* bc_axis, int8_t* bc_sign, double* w,
+                      uint8_t* mask, int64_t* design, int64_t* support, double* A);
+const char* lbgpu_last_create_error(void);
+const char* lbgpu_error_message(const lbgpu_engine* e);
+
+/* --- queries --- */
+/* dims: nx ny nz m mf mt precision exact; counts: nodes design support inlets */
+int lbgpu_info(const lbgpu_engine* e, int* dims, int64_t* counts);
+/* The engine's tables in reference form (for mask parity): any pointer may be NULL. */
+int lbgpu_get_tables(const lbgpu_engine* e, uint8_t* tag, double* bc_T, int8_t* bc_axis,
+                     int8_t* bc_sign, double* w, uint8_t* mask, int64_t* design,
+                     int64_t* support, double* A);
+/* Steps done since creation / the last reset. */
+int lbgpu_counters(const lbgpu_engine* e, int64_t* primal_steps, int64_t* adjoint_steps);
+/* The CUDA stream all work is issued on (cudaStream_t), for event timing. */
+void* lbgpu_stream(const lbgpu_engine* e);
+
+/* --- state (field 0 = primal f, 1 = adjoint v) --- */
+int lbgpu_init_state(lbgpu_engine* e);        /* initialize_state (collision.cpp:296-306), v = 0 */
+int lbgpu_reset_adjoint(lbgpu_engine* e);     /* v.fill(0) (adjoint.cpp:261) */
+int lbgpu_upload_state(lbgpu_engine* e, int field, const double* ref_layout);
+int lbgpu_download_state(lbgpu_engine* e, int field, double* ref_layout);
+/* Device-resident variants: the same layout, pointers to device memory. */
+int lbgpu_upload_state_device(lbgpu_engine* e, int field, const double* d_ref_layout);
+int lbgpu_download_state_device(lbgpu_engine* e, int field, double* d_ref_layout);
+int lbgpu_set_design(lbgpu_engine* e, const double* w_full);   /* DesignField::w (N) */
+int lbgpu_get_design(const lbgpu_engine* e, double* w_full);
+
+/* --- sweeps --- */
+/* n x primal_step (collision.cpp:308-363); residual (nullable) = step_residual
+ * of the last step (collision.cpp:365-375). */
+int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual);
+/* n x adjoint_step (adjoint.cpp:206-254) against the current primal state.
+ * kernel: 0 analytic, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18). */
+int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual);
+/* solve_fixed_point (collision.cpp:377-416): from the current state; tol stop
+ * unless fixed_iters >= 0. Non-finite residual / rho <= 0 -> LBGPU_E_NUMERIC. */
+int lbgpu_solve_primal(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed_iters,
+                       int64_t* iterations, double* residual, int* converged);
+/* solve_adjoint (adjoint.cpp:256-297): v <- 0, then sweeps to tol. */
+int lbgpu_solve_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed_iters,
+                        int kernel, int64_t* iterations, double* residual, int* converged);
+
+/* --- reductions --- */
+/* param_gradient (adjoint.cpp:377-420): g_design in DesignField::nodes
+ * order (n_design), plus the inlet_dp global (nullable). */
+int lbgpu_param_gradient(lbgpu_engine* e, int kernel, double* g_design, double* g_inlet_dp);
+int lbgpu_objective(lbgpu_engine* e, double* value); /* evaluate_raw (objective.cpp:64-72) */
+int lbgpu_penalty(lbgpu_engine* e, double* value);   /* penalty().value (topology.cpp:40-50) */
+
+/* --- design loop --- */
+/* one_shot_run (optimizer.cpp:25-72) for `iterations` iterations with the
+ * per-iteration step size zeta[it-1] and penalty weight lambda[it-1]
+ * (zeta_at / PenaltySchedule::weight_at evaluated by the caller). Rows are
+ * written every record_interval iterations and at the last one. */
+int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta,
+                   const double* lambda, int64_t record_interval, lbgpu_run_row* rows,
+                   int64_t cap, int64_t* n_rows);
+
+/* --- timing (device events on the engine stream; bench support) --- */
+/* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of
+ * `steps` back-to-back sweeps (no residual), bracketed by synchronisation. */
+int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LBGPU_H */

@@ -1,0 +1,309 @@
+"""B200-native LBM primal / discrete-adjoint hot path (arxiv/paper_1501_04741).
+
+Python host mirror of the reference's inner operator seam, over the C ABI in
+include/lbgpu.h (liblbgpu.so, built in-tree by ``build.py``). Method names
+follow the reference operators they replace:
+
+=====================  ===========================================
+``Engine`` method      reference operator (proj/...)
+=====================  ===========================================
+``init_state``         initialize_state (src/collision.cpp:296-306)
+``primal_step``        primal_step + step_residual (:308-375)
+``solve_primal``       solve_fixed_point (:377-416)
+``adjoint_step``       adjoint_step (src/adjoint.cpp:206-254)
+``solve_adjoint``      solve_adjoint (:256-297)
+``param_gradient``     param_gradient (:377-420)
+``objective``          evaluate_raw (src/objective.cpp:64-72)
+``penalty``            penalty (src/topology.cpp:40-50)
+``one_shot``           one_shot_run (src/optimizer.cpp:25-72)
+=====================  ===========================================
+
+Errors raise ``LbgpuError`` carrying the reference's status code
+(lbopt.h:18-25). There is no CPU fallback: without liblbgpu.so or without a
+GPU the constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblbgpu.so")
+
+OK, E_ARG, E_CONFIG, E_NUMERIC, E_IO, E_STATE = range(6)
+
+
+class LbgpuError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class RunRow(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("iteration", "residual", "objective", "penalty",
+                                          "penalty_weight", "composite", "grad_norm")]
+
+
+class SystemDesc(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+        ("precision", C.c_int), ("exact", C.c_int), ("device", C.c_int),
+        ("collision", C.c_int),
+        ("nu", C.c_double), ("beta_fluid", C.c_double), ("beta_solid", C.c_double),
+        ("inlet_dp", C.c_double), ("u_clamp", C.c_double), ("omega_nonhydro", C.c_double),
+        ("switch_theta", C.c_double), ("switch_form", C.c_int),
+        ("A", C.c_void_p), ("relax", C.c_void_p), ("vel", C.c_void_p), ("opp", C.c_void_p),
+        ("tag", C.c_void_p), ("bc_T", C.c_void_p), ("bc_axis", C.c_void_p),
+        ("bc_sign", C.c_void_p), ("w", C.c_void_p), ("design_mask", C.c_void_p),
+        ("obj_kind", C.c_int), ("flux_axis", C.c_int), ("flux_sign", C.c_int),
+        ("support", C.c_void_p), ("n_support", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    from . import build as _b
+    return _b.build(verbose=verbose)
+
+
+def load_library() -> C.CDLL:
+    """Load liblbgpu.so (fails loudly when it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LbgpuError(E_STATE, f"{LIB_PATH} is not built; run paper_1501_04741_b200/build.py")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
+    L.lbgpu_version.restype = C.c_char_p
+    L.lbgpu_last_create_error.restype = C.c_char_p
+    L.lbgpu_error_message.restype = C.c_char_p
+    L.lbgpu_error_message.argtypes = [vp]
+    L.lbgpu_create.argtypes = [C.POINTER(SystemDesc), C.POINTER(vp)]
+    L.lbgpu_create_from_config.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
+    L.lbgpu_destroy.argtypes = [vp]
+    L.lbgpu_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(i64)]
+    L.lbgpu_get_tables.argtypes = [vp] + [vp] * 9
+    L.lbgpu_counters.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+    L.lbgpu_stream.argtypes = [vp]
+    L.lbgpu_stream.restype = vp
+    for name in ("lbgpu_init_state", "lbgpu_reset_adjoint"):
+        getattr(L, name).argtypes = [vp]
+    for name in ("lbgpu_upload_state", "lbgpu_download_state", "lbgpu_upload_state_device",
+                 "lbgpu_download_state_device"):
+        getattr(L, name).argtypes = [vp, C.c_int, vp]
+    L.lbgpu_set_design.argtypes = [vp, vp]
+    L.lbgpu_get_design.argtypes = [vp, vp]
+    L.lbgpu_primal_step.argtypes = [vp, i64, dp]
+    L.lbgpu_adjoint_step.argtypes = [vp, i64, C.c_int, dp]
+    L.lbgpu_solve_primal.argtypes = [vp, C.c_double, i64, i64, C.POINTER(i64), dp,
+                                     C.POINTER(C.c_int)]
+    L.lbgpu_solve_adjoint.argtypes = [vp, C.c_double, i64, i64, C.c_int, C.POINTER(i64), dp,
+                                      C.POINTER(C.c_int)]
+    L.lbgpu_param_gradient.argtypes = [vp, C.c_int, vp, dp]
+    L.lbgpu_objective.argtypes = [vp, dp]
+    L.lbgpu_penalty.argtypes = [vp, dp]
+    L.lbgpu_one_shot.argtypes = [vp, i64, vp, vp, i64, vp, i64, C.POINTER(i64)]
+    L.lbgpu_time_sweeps.argtypes = [vp, C.c_int, i64, dp]
+    _lib = L
+    return L
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Engine:
+    """One lattice on one B200 (see include/lbgpu.h)."""
+
+    def __init__(self, handle: int):
+        self.L = load_library()
+        self.h = C.c_void_p(handle)
+        dims = (C.c_int * 8)()
+        cnt = (C.c_int64 * 4)()
+        self._ok(self.L.lbgpu_info(self.h, dims, cnt))
+        self.shape = (dims[0], dims[1], dims[2])
+        self.m, self.mf, self.mt, self.precision, self.exact = dims[3], dims[4], dims[5], dims[6], dims[7]
+        self.n, self.n_design, self.n_support, self.n_inlets = cnt[0], cnt[1], cnt[2], cnt[3]
+
+    # --- construction -------------------------------------------------------
+    @classmethod
+    def from_config(cls, cfg_text: str, overrides: dict | None = None, device: int = 0,
+                    exact: bool = False) -> "Engine":
+        """CaseConfig text (+ dotted overrides) -> build_case -> engine."""
+        L = load_library()
+        ov = "\n".join(f"{k}={v}" for k, v in (overrides or {}).items()).encode()
+        h = C.c_void_p()
+        rc = L.lbgpu_create_from_config(cfg_text.encode(), ov, device, int(exact), C.byref(h))
+        if rc:
+            raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
+        return cls(h.value)
+
+    @classmethod
+    def from_tables(cls, *, shape, tag, bc_T, bc_axis, bc_sign, w, mask, support,
+                    nu=0.02, beta_fluid=0.003, beta_solid=0.003, inlet_dp=0.0, u_clamp=0.05,
+                    omega_nonhydro=1.0, switch_theta=3.0, fluid_power=False, bgk=False,
+                    obj_kind=0, precision=64, exact=False, device=0, A=None, vel=None,
+                    opp=None) -> "Engine":
+        """Flattened System arrays (the drop-in seam fed by the reference's own
+        System)."""
+        L = load_library()
+        keep = []
+
+        def arr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data
+
+        d = SystemDesc()
+        d.nx, d.ny, d.nz = shape
+        d.precision, d.exact, d.device = precision, int(exact), device
+        d.collision = int(bgk)
+        d.nu, d.beta_fluid, d.beta_solid, d.inlet_dp = nu, beta_fluid, beta_solid, inlet_dp
+        d.u_clamp, d.omega_nonhydro, d.switch_theta = u_clamp, omega_nonhydro, switch_theta
+        d.switch_form = int(fluid_power)
+        d.A = arr(A, np.float64)
+        d.vel = arr(vel, np.int32)
+        d.opp = arr(opp, np.int32)
+        d.tag, d.bc_T = arr(tag, np.uint8), arr(bc_T, np.float64)
+        d.bc_axis, d.bc_sign = arr(bc_axis, np.int8), arr(bc_sign, np.int8)
+        d.w, d.design_mask = arr(w, np.float64), arr(mask, np.uint8)
+        d.obj_kind, d.flux_axis, d.flux_sign = obj_kind, 0, 1
+        d.support = arr(support, np.int64)
+        d.n_support = len(support)
+        h = C.c_void_p()
+        rc = L.lbgpu_create(C.byref(d), C.byref(h))
+        if rc:
+            raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
+        return cls(h.value)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.L.lbgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ok(self, rc: int) -> None:
+        if rc:
+            raise LbgpuError(rc, self.L.lbgpu_error_message(self.h).decode())
+
+    # --- tables / state -------------------------------------------------------
+    def tables(self) -> dict:
+        n = self.n
+        t = {"tag": np.zeros(n, np.uint8), "bc_T": np.zeros(n), "bc_axis": np.zeros(n, np.int8),
+             "bc_sign": np.zeros(n, np.int8), "w": np.zeros(n), "mask": np.zeros(n, np.uint8),
+             "design": np.zeros(max(self.n_design, 1), np.int64),
+             "support": np.zeros(max(self.n_support, 1), np.int64),
+             "A": np.zeros((self.mf, self.mf))}
+        self._ok(self.L.lbgpu_get_tables(self.h, *[_ptr(t[k]) for k in (
+            "tag", "bc_T", "bc_axis", "bc_sign", "w", "mask", "design", "support", "A")]))
+        t["design"] = t["design"][: self.n_design]
+        t["support"] = t["support"][: self.n_support]
+        return t
+
+    def counters(self) -> tuple[int, int]:
+        p, a = C.c_int64(), C.c_int64()
+        self._ok(self.L.lbgpu_counters(self.h, C.byref(p), C.byref(a)))
+        return p.value, a.value
+
+    def stream(self) -> int:
+        return self.L.lbgpu_stream(self.h)
+
+    def init_state(self) -> None:
+        self._ok(self.L.lbgpu_init_state(self.h))
+
+    def reset_adjoint(self) -> None:
+        self._ok(self.L.lbgpu_reset_adjoint(self.h))
+
+    def get_state(self, field: int = 0) -> np.ndarray:
+        out = np.empty(self.m * self.n)
+        self._ok(self.L.lbgpu_download_state(self.h, field, _ptr(out)))
+        return out
+
+    def set_state(self, field: int, data: np.ndarray) -> None:
+        data = np.ascontiguousarray(data, np.float64)
+        assert data.size == self.m * self.n
+        self._ok(self.L.lbgpu_upload_state(self.h, field, _ptr(data)))
+
+    def set_design(self, w_full: np.ndarray) -> None:
+        w_full = np.ascontiguousarray(w_full, np.float64)
+        self._ok(self.L.lbgpu_set_design(self.h, _ptr(w_full)))
+
+    def design(self) -> np.ndarray:
+        out = np.empty(self.n)
+        self._ok(self.L.lbgpu_get_design(self.h, _ptr(out)))
+        return out
+
+    # --- operators --------------------------------------------------------------
+    def primal_step(self, n: int = 1, residual: bool = True) -> float | None:
+        r = C.c_double()
+        self._ok(self.L.lbgpu_primal_step(self.h, n, C.byref(r) if residual else None))
+        return r.value if residual else None
+
+    def adjoint_step(self, n: int = 1, kernel: int = 0, residual: bool = True) -> float | None:
+        r = C.c_double()
+        self._ok(self.L.lbgpu_adjoint_step(self.h, n, kernel, C.byref(r) if residual else None))
+        return r.value if residual else None
+
+    def solve_primal(self, tol: float, max_iter: int = 200000, fixed_iters: int = -1):
+        it, r, cv = C.c_int64(), C.c_double(), C.c_int()
+        self._ok(self.L.lbgpu_solve_primal(self.h, tol, max_iter, fixed_iters, C.byref(it),
+                                           C.byref(r), C.byref(cv)))
+        return it.value, r.value, bool(cv.value)
+
+    def solve_adjoint(self, tol: float, max_iter: int = 200000, fixed_iters: int = -1,
+                      kernel: int = 0):
+        it, r, cv = C.c_int64(), C.c_double(), C.c_int()
+        self._ok(self.L.lbgpu_solve_adjoint(self.h, tol, max_iter, fixed_iters, kernel,
+                                            C.byref(it), C.byref(r), C.byref(cv)))
+        return it.value, r.value, bool(cv.value)
+
+    def param_gradient(self, kernel: int = 0):
+        g = np.zeros(max(self.n_design, 1))
+        gdp = C.c_double()
+        self._ok(self.L.lbgpu_param_gradient(self.h, kernel, _ptr(g), C.byref(gdp)))
+        return g[: self.n_design], gdp.value
+
+    def objective(self) -> float:
+        v = C.c_double()
+        self._ok(self.L.lbgpu_objective(self.h, C.byref(v)))
+        return v.value
+
+    def penalty(self) -> float:
+        v = C.c_double()
+        self._ok(self.L.lbgpu_penalty(self.h, C.byref(v)))
+        return v.value
+
+    def one_shot(self, zeta, lam, record_interval: int = 100) -> np.ndarray:
+        zeta = np.ascontiguousarray(zeta, np.float64)
+        lam = np.ascontiguousarray(lam, np.float64)
+        iters = zeta.size
+        cap = iters // record_interval + 2
+        rows = (RunRow * cap)()
+        nr = C.c_int64()
+        self._ok(self.L.lbgpu_one_shot(self.h, iters, _ptr(zeta), _ptr(lam), record_interval,
+                                       C.addressof(rows), cap, C.byref(nr)))
+        return np.array([[getattr(r, k) for k, _ in RunRow._fields_] for r in rows[: nr.value]])
+
+    def time_sweeps(self, which: int, steps: int) -> float:
+        """Milliseconds of `steps` back-to-back sweeps (CUDA events on the
+        engine stream). which: 0 primal, 1 adjoint."""
+        ms = C.c_double()
+        self._ok(self.L.lbgpu_time_sweeps(self.h, which, steps, C.byref(ms)))
+        return ms.value
+
+
+def version() -> str:
+    return load_library().lbgpu_version().decode()

@@ -1,0 +1,1030 @@
+// lbgpu engine: device memory, sweep orchestration and the C ABI of
+// include/lbgpu.h. One engine = one lattice on one GPU, all work on one
+// stream. The node kernels live in kernels.cuh (fast build and bit-exact
+// build); this file owns the buffers, the solve/stop logic of the
+// reference's drivers, the deterministic pairwise reductions and the error
+// conventions of its C API.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lbgpu.h"
+#include "casebuild.h"
+#include "types.cuh"
+
+namespace lbgpu {
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CU(call)                                                                         \
+  do {                                                                                   \
+    const cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                               \
+      throw Fail{LBGPU_E_NUMERIC, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                      " (" #call ")"};                                   \
+  } while (0)
+
+constexpr unsigned long long kNoBad = ~0ull;
+constexpr unsigned long long kIdxMask = (1ull << 40) - 1;
+
+// ------------------------------------------------------------ tables
+// Full-pivot Gauss-Jordan inverse (the same elimination order as the oracle
+// build's Eigen stand-in, so A agrees bit-for-bit with oracle/_ref; it agrees
+// with the reference's Eigen FullPivLU to round-off).
+bool invert(const std::vector<double>& m, int n, std::vector<double>& out) {
+  std::vector<double> a = m, inv(size_t(n) * n, 0.0);
+  std::vector<int> colperm(n);
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0, colperm[i] = i;
+  double det = 1.0;
+  for (int k = 0; k < n; ++k) {
+    int pr = k, pc = k;
+    double best = -1.0;
+    for (int i = k; i < n; ++i)
+      for (int j = k; j < n; ++j)
+        if (std::abs(a[i * n + j]) > best) best = std::abs(a[i * n + j]), pr = i, pc = j;
+    if (!(best > 0.0)) return false;
+    if (pr != k) {
+      for (int j = 0; j < n; ++j) std::swap(a[pr * n + j], a[k * n + j]), std::swap(inv[pr * n + j], inv[k * n + j]);
+      det = -det;
+    }
+    if (pc != k) {
+      for (int i = 0; i < n; ++i) std::swap(a[i * n + pc], a[i * n + k]);
+      std::swap(colperm[pc], colperm[k]);
+      det = -det;
+    }
+    const double p = a[k * n + k];
+    det *= p;
+    for (int j = 0; j < n; ++j) a[k * n + j] /= p, inv[k * n + j] /= p;
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = a[i * n + k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) a[i * n + j] -= f * a[k * n + j], inv[i * n + j] -= f * inv[k * n + j];
+    }
+  }
+  if (!(std::abs(det) > 1e-12)) return false;
+  out.assign(size_t(n) * n, 0.0);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j) out[colperm[k] * n + j] = inv[k * n + j];
+  return true;
+}
+
+// operator* with the reference's loop order and zero skip (matrix.cpp:24-33).
+std::vector<double> matmul(const std::vector<double>& l, const std::vector<double>& r, int n) {
+  std::vector<double> out(size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      const double v = l[i * n + k];
+      if (v == 0.0) continue;
+      for (int j = 0; j < n; ++j) out[i * n + j] += v * r[k * n + j];
+    }
+  return out;
+}
+
+template <class L>
+void model_rows(std::vector<double>& U, std::vector<int>& cls) {
+  U.assign(L::MF * L::MF, 0.0);
+  cls.assign(L::MF, 0);
+  for (int i = 0; i < L::MF; ++i) {
+    cls[i] = L::row_class(i);
+    for (int j = 0; j < L::MF; ++j) U[i * L::MF + j] = L::U(i, j);
+  }
+}
+
+// ------------------------------------------------------- pairwise tree
+// pairwise_sum_fn (reduce.hpp:43-52): leaves of <= 16 terms from midpoint
+// splits, combined in the recursion's post-order. The shape depends only on
+// n, so it is built once on the host and replayed on the device.
+struct PairTree {
+  long long n = -1;
+  int leaves = 0, ops = 0;
+  long long* d_lo = nullptr;
+  long long* d_hi = nullptr;
+  int2* d_ops = nullptr;
+  double* d_vals = nullptr;
+
+  void build(long long count) {
+    release();
+    n = count;
+    std::vector<long long> lo, hi;
+    std::vector<std::pair<int, int>> tmp;  // encoded child ids
+    std::function<int(long long, long long)> rec = [&](long long a, long long b) -> int {
+      if (b - a <= 16) {
+        lo.push_back(a);
+        hi.push_back(b);
+        return int(lo.size() - 1);  // leaf id >= 0
+      }
+      const long long mid = a + (b - a) / 2;
+      const int x = rec(a, mid), y = rec(mid, b);
+      tmp.push_back({x, y});
+      return -int(tmp.size());  // internal id -k (k = 1-based post-order)
+    };
+    rec(0, count);
+    leaves = int(lo.size());
+    ops = int(tmp.size());
+    auto dec = [&](int id) { return id >= 0 ? id : leaves + (-id - 1); };
+    std::vector<int2> o(ops);
+    for (int k = 0; k < ops; ++k) o[k] = make_int2(dec(tmp[k].first), dec(tmp[k].second));
+    CU(cudaMalloc(&d_lo, sizeof(long long) * leaves));
+    CU(cudaMalloc(&d_hi, sizeof(long long) * leaves));
+    CU(cudaMalloc(&d_vals, sizeof(double) * (leaves + ops + 1)));
+    CU(cudaMemcpy(d_lo, lo.data(), sizeof(long long) * leaves, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_hi, hi.data(), sizeof(long long) * leaves, cudaMemcpyHostToDevice));
+    if (ops) {
+      CU(cudaMalloc(&d_ops, sizeof(int2) * ops));
+      CU(cudaMemcpy(d_ops, o.data(), sizeof(int2) * ops, cudaMemcpyHostToDevice));
+    }
+  }
+  void release() {
+    cudaFree(d_lo), cudaFree(d_hi), cudaFree(d_ops), cudaFree(d_vals);
+    d_lo = d_hi = nullptr, d_ops = nullptr, d_vals = nullptr, n = -1;
+  }
+};
+
+__global__ void k_leaf_sums(const double* __restrict__ t, const long long* lo, const long long* hi,
+                            int leaves, double* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= leaves) return;
+  double s = 0.0;
+  for (long long k = lo[i]; k < hi[i]; ++k) s += t[k];
+  vals[i] = s;
+}
+
+// Post-order combine; a single thread keeps the reference's exact order.
+__global__ void k_combine(double* vals, const int2* ops, int leaves, int nops, double* out) {
+  for (int k = 0; k < nops; ++k) vals[leaves + k] = vals[ops[k].x] + vals[ops[k].y];
+  *out = nops ? vals[leaves + nops - 1] : vals[0];
+}
+
+__global__ void k_penalty_terms(const double* __restrict__ w, const long long* __restrict__ nodes,
+                                long long n, double* __restrict__ t) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double wi = w[nodes[i]];
+  t[i] = wi * (1.0 - wi);  // topology.cpp:46-49
+}
+
+}  // namespace
+}  // namespace lbgpu
+
+using namespace lbgpu;
+
+struct lbgpu_engine {
+  // shape / mode
+  int nx = 0, ny = 0, nz = 0, dim = 2, mf = 0, mt = 0, m = 0, prec = 64, exact = 0, ck = 0;
+  long long N = 0;
+  int device = 0;
+  Model M{};
+  NodeTables T{};
+  Geom G{};
+  // host copies
+  std::vector<uint8_t> tag, mask, code;
+  std::vector<double> w, bc_T, A, relax;
+  std::vector<int8_t> bc_axis, bc_sign;
+  std::vector<long long> design, support, inlets;
+  // device
+  void* f[2] = {nullptr, nullptr};
+  void* v[2] = {nullptr, nullptr};
+  void* snap = nullptr;  // rollback copy for exact tol-stop in batched solves
+  int fc = 0, vc = 0;
+  uint8_t* d_code = nullptr;
+  double *d_w = nullptr, *d_bcT = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
+  double *d_A = nullptr, *d_At = nullptr;
+  long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr;
+  double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
+  double* d_ref = nullptr;
+  unsigned long long* d_flags = nullptr;  // [resid, bad, aux]
+  unsigned long long* d_ring = nullptr;   // per-step residual ring for batched solves
+  unsigned long long* h_flags = nullptr;  // pinned mirror
+  PairTree tree_support, tree_design, tree_inlet;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long primal_steps = 0, adjoint_steps = 0;
+  std::string err;
+
+  size_t bytes_per_real() const { return prec == 64 ? 8 : 4; }
+  size_t field_bytes() const { return bytes_per_real() * size_t(m) * size_t(N); }
+
+  ~lbgpu_engine() {
+    if (!st) return;  // host-only instance (lbgpu_case_tables)
+    if (device >= 0) cudaSetDevice(device);
+    for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
+    cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
+    cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
+    cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
+    cudaFree(d_ring);
+    if (h_flags) cudaFreeHost(h_flags);
+    tree_support.release(), tree_design.release(), tree_inlet.release();
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  // ------------------------------------------------------------ setup
+  // Host half: validation, tables, node codes (no CUDA calls).
+  void setup_host(const lbgpu_system_desc& d) {
+    if (d.nx < 1 || d.ny < 1 || d.nz < 1) throw Fail{LBGPU_E_CONFIG, "lattice extents must be positive"};
+    if (d.precision != 64 && d.precision != 32) throw Fail{LBGPU_E_CONFIG, "precision must be 32 or 64"};
+    if (d.exact && d.precision != 64)
+      throw Fail{LBGPU_E_CONFIG, "the bit-exact build is double precision only"};
+    if (!d.tag || !d.bc_T || !d.bc_axis || !d.bc_sign || !d.w || !d.design_mask || !d.support)
+      throw Fail{LBGPU_E_ARG, "system description is missing a per-node table"};
+    nx = d.nx, ny = d.ny, nz = d.nz, prec = d.precision, exact = d.exact ? 1 : 0;
+    device = d.device;
+    N = (long long)nx * ny * nz;
+    dim = nz == 1 ? 2 : 3;
+    mf = dim == 2 ? LatD2::MF : LatD3::MF;
+    mt = dim == 2 ? LatD2::MT : LatD3::MT;
+    m = mf + mt;
+    if (d.vel || d.opp) check_lattice(d);
+    if (!(d.nu > 0)) throw Fail{LBGPU_E_CONFIG, "viscosity must be positive"};
+    if (d.beta_fluid < 0 || d.beta_solid < 0) throw Fail{LBGPU_E_CONFIG, "diffusivities must be non-negative"};
+    if (!(d.u_clamp > 0)) throw Fail{LBGPU_E_CONFIG, "velocity clamp must be positive"};
+    if (!(d.switch_theta > 0)) throw Fail{LBGPU_E_CONFIG, "switching exponent must be positive"};
+    build_model(d);
+    // tags (TagMap::validate, collision.cpp:8-23)
+    tag.assign(d.tag, d.tag + N);
+    bc_T.assign(d.bc_T, d.bc_T + N);
+    bc_axis.assign(d.bc_axis, d.bc_axis + N);
+    bc_sign.assign(d.bc_sign, d.bc_sign + N);
+    w.assign(d.w, d.w + N);
+    mask.assign(d.design_mask, d.design_mask + N);
+    for (long long i = 0; i < N; ++i) {
+      if (tag[i] > 4) throw Fail{LBGPU_E_CONFIG, "unknown node tag"};
+      if (tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) {
+        if (bc_axis[i] < 0 || bc_axis[i] > 2 || (dim == 2 && bc_axis[i] == 2))
+          throw Fail{LBGPU_E_CONFIG, "pressure node has a normal off the lattice axes"};
+        if (bc_sign[i] != 1 && bc_sign[i] != -1)
+          throw Fail{LBGPU_E_CONFIG, "pressure node normal sign must be +1 or -1"};
+      }
+      if (!std::isfinite(bc_T[i])) throw Fail{LBGPU_E_CONFIG, "prescribed temperature is not finite"};
+      if (mask[i]) design.push_back(i);
+      if (tag[i] == TAG_INLET) inlets.push_back(i);
+    }
+    M.obj_kind = d.obj_kind, M.flux_axis = d.flux_axis, M.flux_sign = d.flux_sign;
+    if (d.obj_kind < 0 || d.obj_kind > 2) throw Fail{LBGPU_E_CONFIG, "unknown objective kind"};
+    support.assign(d.support, d.support + d.n_support);
+    for (size_t k = 0; k < support.size(); ++k)
+      if (support[k] < 0 || support[k] >= N || (k && support[k] <= support[k - 1]))
+        throw Fail{LBGPU_E_CONFIG, "objective support must be ascending node indices"};
+    build_codes();
+  }
+
+  void setup(const lbgpu_system_desc& d) {
+    setup_host(d);
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&ev0));
+    CU(cudaEventCreate(&ev1));
+    const size_t fb = field_bytes();
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaMalloc(&f[b], fb));
+      CU(cudaMalloc(&v[b], fb));
+      CU(cudaMemset(v[b], 0, fb));
+    }
+    CU(cudaMalloc(&d_code, N));
+    CU(cudaMalloc(&d_w, sizeof(double) * N));
+    CU(cudaMalloc(&d_bcT, sizeof(double) * N));
+    CU(cudaMemcpy(d_code, code.data(), N, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_w, w.data(), sizeof(double) * N, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_bcT, bc_T.data(), sizeof(double) * N, cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&d_A, sizeof(double) * mf * mf));
+    CU(cudaMalloc(&d_At, sizeof(double) * mf * mf));
+    std::vector<double> At(size_t(mf) * mf);
+    for (int i = 0; i < mf; ++i)
+      for (int j = 0; j < mf; ++j) At[j * mf + i] = A[i * mf + j];
+    CU(cudaMemcpy(d_A, A.data(), sizeof(double) * mf * mf, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_At, At.data(), sizeof(double) * mf * mf, cudaMemcpyHostToDevice));
+    M.A = d_A, M.At = d_At;
+    auto up_list = [&](const std::vector<long long>& h, long long*& dptr) {
+      CU(cudaMalloc(&dptr, sizeof(long long) * std::max<size_t>(h.size(), 1)));
+      if (!h.empty())
+        CU(cudaMemcpy(dptr, h.data(), sizeof(long long) * h.size(), cudaMemcpyHostToDevice));
+    };
+    up_list(design, d_design);
+    up_list(support, d_support);
+    up_list(inlets, d_inlets);
+    const size_t nt = std::max({design.size(), support.size(), inlets.size(), size_t(1)});
+    CU(cudaMalloc(&d_terms, sizeof(double) * nt));
+    CU(cudaMalloc(&d_grad, sizeof(double) * std::max<size_t>(design.size(), 1)));
+    CU(cudaMalloc(&d_scalar, sizeof(double) * 4));
+    CU(cudaMalloc(&d_flags, sizeof(unsigned long long) * 4));
+    CU(cudaMalloc(&d_ring, sizeof(unsigned long long) * kRing));
+    CU(cudaMallocHost(&h_flags, sizeof(unsigned long long) * (4 + kRing)));
+    tree_support.build((long long)support.size());
+    tree_design.build((long long)design.size());
+    tree_inlet.build((long long)inlets.size());
+    reset_flags();
+    if (exact) {
+      CU(cudaMalloc(&d_p0, sizeof(double) * N));
+      CU(cudaMalloc(&d_p1, sizeof(double) * N));
+      refresh_pow_tables();
+    }
+    T.code = d_code, T.w = d_w, T.bcT = d_bcT, T.p0 = d_p0, T.p1 = d_p1;
+    G = Geom{nx, ny, nz, 0, nx, N, 0, nx, ny};
+    init_state();
+    CU(cudaStreamSynchronize(st));
+  }
+
+  static constexpr int kRing = 64;
+
+  void check_lattice(const lbgpu_system_desc& d) {
+    for (int p = 0; p < m; ++p) {
+      const int e0 = dim == 2 ? cvel<LatD2>(p, 0) : cvel<LatD3>(p, 0);
+      const int e1 = dim == 2 ? cvel<LatD2>(p, 1) : cvel<LatD3>(p, 1);
+      const int e2 = dim == 2 ? cvel<LatD2>(p, 2) : cvel<LatD3>(p, 2);
+      const int o = dim == 2 ? copp<LatD2>(p) : copp<LatD3>(p);
+      if (d.vel && (d.vel[3 * p] != e0 || d.vel[3 * p + 1] != e1 || d.vel[3 * p + 2] != e2))
+        throw Fail{LBGPU_E_CONFIG, "coupled velocity table does not match the engine's lattice"};
+      if (d.opp && d.opp[p] != o)
+        throw Fail{LBGPU_E_CONFIG, "coupled opposite map does not match the engine's lattice"};
+    }
+  }
+
+  // ModelTables::build (collision.cpp:46-71) and the fast-path factors.
+  void build_model(const lbgpu_system_desc& d) {
+    const double om = 1.0 / (0.5 + 3.0 * d.nu);
+    std::vector<double> U;
+    std::vector<int> cls;
+    if (dim == 2) model_rows<LatD2>(U, cls);
+    else model_rows<LatD3>(U, cls);
+    const bool bgk = d.collision == 1;
+    if (d.relax) {
+      relax.assign(d.relax, d.relax + mf);
+    } else if (bgk) {
+      relax.assign(mf, om);
+    } else {
+      relax.assign(mf, d.omega_nonhydro);
+      for (int i = 0; i < mf; ++i) {
+        if (cls[i] == 1) relax[i] = om;
+        if (cls[i] == 0) relax[i] = 1.0;
+      }
+    }
+    if (d.A) {
+      A.assign(d.A, d.A + mf * mf);
+    } else {
+      std::vector<double> Ub, Ubinv;
+      if (bgk) {
+        Ub.assign(mf * mf, 0.0);
+        for (int i = 0; i < mf; ++i) Ub[i * mf + i] = 1.0;
+        Ubinv = Ub;
+      } else {
+        Ub = U;
+        if (!invert(Ub, mf, Ubinv)) throw Fail{LBGPU_E_CONFIG, "matrix not invertible (|det| <= tolerance)"};
+      }
+      std::vector<double> imt(mf * mf, 0.0);
+      for (int i = 0; i < mf; ++i) imt[i * mf + i] = 1.0 - relax[i];
+      A = matmul(Ubinv, matmul(imt, Ub, mf), mf);
+    }
+    M.om = om;
+    M.beta_f = d.beta_fluid, M.beta_s = d.beta_solid;
+    M.rho_in = 1.0 + 3.0 * d.inlet_dp;
+    M.rho_out = 1.0;
+    M.u_clamp = d.u_clamp;
+    M.theta = d.switch_theta;
+    M.theta_int = (d.switch_theta == std::floor(d.switch_theta) && d.switch_theta >= 1 &&
+                   d.switch_theta <= 16) ? int(d.switch_theta) : 0;
+    M.fluid_power = d.switch_form == 1;
+    M.collision_bgk = bgk;
+    // Fast MRT: A = U^T diag(c) U with c_i = (1 - relax_i)/|U_i|^2 needs
+    // mutually orthogonal moment rows; both bases are.
+    M.nonhydro = 0;
+    for (int i = 0; i < mf; ++i) {
+      double n2 = 0.0;
+      for (int j = 0; j < mf; ++j) n2 += U[i * mf + j] * U[i * mf + j];
+      M.mrt_c[i] = (1.0 - relax[i]) / n2;
+      if (cls[i] == 2 && relax[i] != 1.0) M.nonhydro = 1;
+      for (int k = 0; k < i; ++k) {
+        double dot = 0.0;
+        for (int j = 0; j < mf; ++j) dot += U[i * mf + j] * U[k * mf + j];
+        if (std::abs(dot) > 1e-12) throw Fail{LBGPU_E_CONFIG, "moment basis is not orthogonal"};
+      }
+    }
+    ck = bgk ? 0 : (M.nonhydro ? 2 : 1);
+    // Non-design nodes (w == 1): the pow pair and thermal rate are constants.
+    const double base1 = M.fluid_power ? 1.0 : 0.0;
+    T.pp_one = {std::pow(base1, M.theta), std::pow(base1, M.theta - 1.0)};
+    if (prec == 64) {
+      const double beta = 1.0 * M.beta_f + (1.0 - 1.0) * M.beta_s;
+      T.omt_one = 1.0 / (0.5 + 3.0 * beta);
+    } else {
+      const float wf = 1.0f, beta = wf * float(M.beta_f) + (1.0f - wf) * float(M.beta_s);
+      T.omt_one = double(1.0f / (0.5f + 3.0f * beta));
+    }
+  }
+
+  void build_codes() {
+    code.assign(N, 0);
+    std::vector<uint8_t> on_support(N, 0);
+    for (long long i : support) on_support[i] = 1;
+    for (long long i = 0; i < N; ++i) {
+      uint8_t c = tag[i];
+      if (mask[i] || w[i] != 1.0) c |= CODE_HAS_W;
+      if (on_support[i]) c |= CODE_SUPPORT;
+      if (tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) {
+        c |= uint8_t(bc_axis[i] << CODE_AXIS_SHIFT);
+        if (bc_sign[i] < 0) c |= CODE_NEG;
+      }
+      code[i] = c;
+    }
+  }
+
+  // Exact build: pow(base, theta) / pow(base, theta-1) from the host libm,
+  // exactly the calls switching_eval / switching_derivative / pow(Dual) make
+  // (topology.hpp:42-46, topology.cpp:34-38, dual.hpp:56-61).
+  void refresh_pow_tables() {
+    std::vector<double> p0(N, 0.0), p1(N, 0.0);
+    for (long long i = 0; i < N; ++i) {
+      if (!(code[i] & CODE_HAS_W)) continue;
+      const double base = M.fluid_power ? w[i] : 1.0 - w[i];
+      p0[i] = std::pow(base, M.theta);
+      p1[i] = std::pow(base, M.theta - 1.0);
+    }
+    CU(cudaMemcpyAsync(d_p0, p0.data(), sizeof(double) * N, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_p1, p1.data(), sizeof(double) * N, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+  }
+
+  // ------------------------------------------------------------ helpers
+  void reset_flags() {
+    const unsigned long long init[4] = {0ull, kNoBad, 0ull, 0ull};
+    CU(cudaMemcpyAsync(d_flags, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  }
+  Launch launch(unsigned long long step) const {
+    Launch a;
+    a.g = G;
+    a.t = T;
+    a.M = M;
+    a.fl.resid = d_flags;
+    a.fl.bad = d_flags + 1;
+    a.fl.aux = d_flags + 2;
+    a.fl.step_key = step << 40;
+    a.stream = st;
+    return a;
+  }
+  SweepArgs sweep(unsigned long long step, bool resid, unsigned long long* resid_slot) const {
+    SweepArgs s;
+    s.a = launch(step);
+    if (resid_slot) s.a.fl.resid = resid_slot;
+    s.dim = dim, s.prec = prec, s.ck = ck, s.resid = resid;
+    return s;
+  }
+  void sync() { CU(cudaStreamSynchronize(st)); }
+  void pull_flags() {
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+    sync();
+  }
+  // NumericError with the reference's message shape (collision.cpp:355-361, 387-389).
+  void raise_bad(unsigned long long key, const char* what) {
+    const long long gidx = (long long)(key & kIdxMask);
+    const long long step = (long long)(key >> 40);
+    const int x = int(gidx % nx), y = int((gidx / nx) % ny), z = int(gidx / ((long long)nx * ny));
+    reset_flags();
+    throw Fail{LBGPU_E_NUMERIC, "non-positive density at node (" + std::to_string(x) + "," +
+                                    std::to_string(y) + "," + std::to_string(z) + ") (" + what +
+                                    " " + std::to_string(step) + ")"};
+  }
+  void check_bad(const char* what) {
+    pull_flags();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], what);
+  }
+  static double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+  }
+
+  // ------------------------------------------------------------ sweeps
+  void primal_launch(bool resid, unsigned long long* slot) {
+    ++primal_steps;
+    const SweepArgs s = sweep(primal_steps, resid, slot);
+    if (exact) exact::primal(s, f[fc], f[1 - fc]);
+    else fast::primal(s, f[fc], f[1 - fc]);
+    fc ^= 1;
+  }
+  void adjoint_launch(int kernel, bool resid, unsigned long long* slot) {
+    ++adjoint_steps;
+    const SweepArgs s = sweep(adjoint_steps, resid, slot);
+    if (kernel) {
+      if (exact) exact::adjoint_dual(s, f[fc], v[vc], v[1 - vc]);
+      else fast::adjoint_dual(s, f[fc], v[vc], v[1 - vc]);
+    } else {
+      if (exact) exact::adjoint(s, f[fc], v[vc], v[1 - vc]);
+      else fast::adjoint(s, f[fc], v[vc], v[1 - vc]);
+    }
+    vc ^= 1;
+  }
+
+  void init_state() {
+    if (exact) exact::init_state(N, dim, prec, f[fc], st);
+    else fast::init_state(N, dim, prec, f[fc], st);
+    CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
+    CU(cudaGetLastError());
+  }
+
+  double steps(int which, long long n, int kernel, bool want_resid) {
+    if (n <= 0) return 0.0;
+    reset_flags();
+    for (long long k = 0; k < n; ++k) {
+      const bool r = want_resid && k == n - 1;
+      if (which == 0) primal_launch(r, nullptr);
+      else adjoint_launch(kernel, r, nullptr);
+    }
+    CU(cudaGetLastError());
+    pull_flags();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], which == 0 ? "iteration" : "adjoint iteration");
+    return want_resid ? bits_to_double(h_flags[0]) : 0.0;
+  }
+
+  // solve_fixed_point / solve_adjoint stop rule (collision.cpp:377-416,
+  // adjoint.cpp:256-297), batched: every step writes its residual into a ring
+  // slot, the host scans once per batch, and an overshoot past the first
+  // r <= tol is undone from a snapshot and replayed, so the stop iteration
+  // and final state are exactly the per-step loop's.
+  void solve(int which, double tol, long long max_iter, long long fixed, int kernel,
+             long long* iters, double* resid, int* conv) {
+    const long long n = fixed >= 0 ? fixed : max_iter;
+    const char* what = which == 0 ? "iteration" : "adjoint iteration";
+    if (which == 1) {
+      CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
+      CU(cudaMemsetAsync(v[1 - vc], 0, field_bytes(), st));
+    }
+    if (fixed < 0 && !snap) CU(cudaMalloc(&snap, field_bytes()));
+    reset_flags();
+    long long it = 0;
+    double r = 0.0;
+    long long batch = 1;
+    while (it < n) {
+      const long long b = std::min<long long>({batch, n - it, (long long)kRing});
+      void** buf = which == 0 ? f : v;
+      int& cur = which == 0 ? fc : vc;
+      const int cur0 = cur;
+      const long long steps0 = which == 0 ? primal_steps : adjoint_steps;
+      if (fixed < 0 && b > 1) CU(cudaMemcpyAsync(snap, buf[cur], field_bytes(), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long) * b, st));
+      for (long long k = 0; k < b; ++k) {
+        if (which == 0) primal_launch(true, d_ring + k);
+        else adjoint_launch(kernel, true, d_ring + k);
+      }
+      CU(cudaGetLastError());
+      CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long) * b, cudaMemcpyDeviceToHost, st));
+      sync();
+      // first failing step in the batch, in step order
+      long long stop = -1;
+      for (long long k = 0; k < b; ++k) {
+        const double rk = bits_to_double(h_flags[4 + k]);
+        const long long itk = it + k + 1;
+        const bool badk = h_flags[1] != kNoBad && (long long)(h_flags[1] >> 40) == steps0 + k + 1;
+        if (badk) raise_bad(h_flags[1], what);
+        if (!std::isfinite(rk)) {
+          reset_flags();
+          throw Fail{LBGPU_E_NUMERIC, std::string(which == 0 ? "state" : "adjoint") +
+                                          " diverged (non-finite residual) at iteration " +
+                                          std::to_string(itk)};
+        }
+        if (fixed < 0 && rk <= tol) {
+          stop = k;
+          r = rk;
+          break;
+        }
+      }
+      if (stop >= 0) {
+        if (stop < b - 1) {  // roll back and replay exactly stop+1 steps
+          CU(cudaMemcpyAsync(buf[cur0], snap, field_bytes(), cudaMemcpyDeviceToDevice, st));
+          cur = cur0;
+          if (which == 0) primal_steps = steps0;
+          else adjoint_steps = steps0;
+          for (long long k = 0; k <= stop; ++k) {
+            if (which == 0) primal_launch(false, nullptr);
+            else adjoint_launch(kernel, false, nullptr);
+          }
+          sync();
+        }
+        it += stop + 1;
+        break;
+      }
+      it += b;
+      r = bits_to_double(h_flags[4 + b - 1]);
+      batch = std::min<long long>(batch * 2, kRing);
+    }
+    *iters = it;
+    *resid = r;
+    *conv = r <= tol;
+  }
+
+  // ------------------------------------------------------- reductions
+  double pairwise(PairTree& tr, const double* d_t) {
+    const int nb = (tr.leaves + 127) / 128;
+    k_leaf_sums<<<nb, 128, 0, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_vals);
+    k_combine<<<1, 1, 0, st>>>(tr.d_vals, tr.d_ops, tr.leaves, tr.ops, d_scalar);
+    double out = 0.0;
+    CU(cudaMemcpyAsync(&out, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();
+    return out;
+  }
+  double objective() {
+    reset_flags();
+    const Launch a = launch(primal_steps);
+    if (exact) exact::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms);
+    else fast::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms);
+    CU(cudaGetLastError());
+    const double val = pairwise(tree_support, d_terms);
+    check_bad("iteration");
+    return val;
+  }
+  double penalty() {
+    const long long n = (long long)design.size();
+    if (n) k_penalty_terms<<<unsigned((n + 127) / 128), 128, 0, st>>>(d_w, d_design, n, d_terms);
+    CU(cudaGetLastError());
+    return pairwise(tree_design, d_terms);
+  }
+  void gradient(int kernel, double* g, double* gdp) {
+    reset_flags();
+    const Launch a = launch(adjoint_steps);
+    const long long n = (long long)design.size();
+    if (exact) exact::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0);
+    else fast::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0);
+    CU(cudaGetLastError());
+    if (g && n) CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (gdp) {
+      const long long ni = (long long)inlets.size();
+      if (exact) exact::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms);
+      else fast::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms);
+      CU(cudaGetLastError());
+      *gdp = pairwise(tree_inlet, d_terms);
+    }
+    check_bad("gradient at iteration");
+  }
+
+  void one_shot(long long iters, const double* zeta, const double* lambda, long long ri,
+                lbgpu_run_row* rows, long long cap, long long* nrows) {
+    long long k = 0;
+    reset_flags();
+    const long long n = (long long)design.size();
+    for (long long it = 1; it <= iters; ++it) {
+      const bool rec = (it % ri == 0) || it == iters;
+      if (rec) CU(cudaMemsetAsync(d_flags, 0, sizeof(unsigned long long), st));
+      primal_launch(rec, nullptr);
+      adjoint_launch(0, false, nullptr);
+      if (rec) CU(cudaMemsetAsync(d_flags + 2, 0, sizeof(unsigned long long), st));
+      const Launch a = launch(adjoint_steps);
+      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1]);
+      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1]);
+      CU(cudaGetLastError());
+      if (exact) {  // the device moved w: refresh the host copy and the libm pow tables
+        CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+        sync();
+        refresh_pow_tables();
+      }
+      if (rec) {
+        pull_flags();
+        if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+        lbgpu_run_row row;
+        row.iteration = double(it);
+        row.residual = bits_to_double(h_flags[0]);
+        const double gn = bits_to_double(h_flags[2]);
+        row.objective = objective();
+        row.penalty = penalty();
+        row.penalty_weight = lambda[it - 1];
+        row.composite = row.objective - lambda[it - 1] * row.penalty;
+        row.grad_norm = gn;
+        if (k < cap && rows) rows[k] = row;
+        ++k;
+      }
+    }
+    if (!exact) CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    sync();
+    check_bad("iteration");
+    *nrows = k;
+  }
+
+  // ------------------------------------------------------------ layout
+  void to_ref(int field, double* d_out) {
+    void* buf = field == 0 ? f[fc] : v[vc];
+    if (exact) exact::layout(G, dim, prec, field, true, buf, d_out, st);
+    else fast::layout(G, dim, prec, field, true, buf, d_out, st);
+    CU(cudaGetLastError());
+  }
+  void from_ref(int field, const double* d_in) {
+    void* buf = field == 0 ? f[fc] : v[vc];
+    if (exact) exact::layout(G, dim, prec, field, false, d_in, buf, st);
+    else fast::layout(G, dim, prec, field, false, d_in, buf, st);
+    CU(cudaGetLastError());
+  }
+  void ensure_ref() {
+    if (!d_ref) CU(cudaMalloc(&d_ref, sizeof(double) * size_t(m) * N));
+  }
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class F>
+int guarded(lbgpu_engine* e, F&& fn) {
+  if (!e) return LBGPU_E_ARG;
+  try {
+    if (e->device >= 0) cudaSetDevice(e->device);
+    fn();
+    e->err.clear();
+    return LBGPU_OK;
+  } catch (const Fail& f) {
+    e->err = f.msg;
+    return f.code;
+  } catch (const std::exception& x) {
+    e->err = x.what();
+    return LBGPU_E_NUMERIC;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lbgpu_version(void) { return "0.1.0-b200"; }
+
+int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out) {
+  if (!desc || !out) return LBGPU_E_ARG;
+  *out = nullptr;
+  g_create_err.clear();
+  auto* e = new lbgpu_engine();
+  try {
+    e->setup(*desc);
+    *out = e;
+    return LBGPU_OK;
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    delete e;
+    return f.code;
+  } catch (const std::exception& x) {
+    g_create_err = x.what();
+    delete e;
+    return LBGPU_E_NUMERIC;
+  }
+}
+
+static int desc_from_config(const char* cfg_text, const char* overrides, int device, int exact,
+                            CaseSpec& c, SystemArrays& s, lbgpu_system_desc& d) {
+  std::string err;
+  if (!parse_case(cfg_text, overrides ? overrides : "", c, err) || !build_system(c, s, err)) {
+    g_create_err = err;
+    return LBGPU_E_CONFIG;
+  }
+  d = lbgpu_system_desc{};
+  d.nx = c.nx, d.ny = c.ny, d.nz = c.nz;
+  d.precision = c.precision;
+  d.exact = exact;
+  d.device = device;
+  d.collision = c.collision == "bgk" ? 1 : 0;
+  d.nu = c.nu, d.beta_fluid = c.beta_fluid, d.beta_solid = c.beta_solid;
+  d.inlet_dp = c.inlet_dp, d.u_clamp = c.u_clamp, d.omega_nonhydro = c.omega_nonhydro;
+  d.switch_theta = c.switch_theta;
+  d.switch_form = c.switch_form == "fluid_power" ? 1 : 0;
+  d.tag = s.tag.data(), d.bc_T = s.bc_T.data(), d.bc_axis = s.bc_axis.data();
+  d.bc_sign = s.bc_sign.data(), d.w = s.w.data(), d.design_mask = s.mask.data();
+  d.obj_kind = s.obj_kind, d.flux_axis = s.flux_axis, d.flux_sign = s.flux_sign;
+  d.support = s.support.data(), d.n_support = (int64_t)s.support.size();
+  return LBGPU_OK;
+}
+
+int lbgpu_create_from_config(const char* cfg_text, const char* overrides, int device, int exact,
+                             lbgpu_engine** out) {
+  if (!cfg_text || !out) return LBGPU_E_ARG;
+  *out = nullptr;
+  g_create_err.clear();
+  CaseSpec c;
+  SystemArrays s;
+  lbgpu_system_desc d;
+  const int rc = desc_from_config(cfg_text, overrides, device, exact, c, s, d);
+  if (rc) return rc;
+  return lbgpu_create(&d, out);
+}
+
+int lbgpu_case_tables(const char* cfg_text, const char* overrides, int* dims, int64_t* counts,
+                      uint8_t* tag, double* bc_T, int8_t* bc_axis, int8_t* bc_sign, double* w,
+                      uint8_t* mask, int64_t* design, int64_t* support, double* A) {
+  if (!cfg_text || !dims || !counts) return LBGPU_E_ARG;
+  g_create_err.clear();
+  CaseSpec c;
+  SystemArrays s;
+  lbgpu_system_desc d;
+  const int rc = desc_from_config(cfg_text, overrides, 0, 0, c, s, d);
+  if (rc) return rc;
+  lbgpu_engine e;
+  try {
+    e.setup_host(d);
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    return f.code;
+  }
+  const int dd[8] = {e.nx, e.ny, e.nz, e.m, e.mf, e.mt, e.prec, 0};
+  std::memcpy(dims, dd, sizeof dd);
+  counts[0] = e.N;
+  counts[1] = (int64_t)e.design.size();
+  counts[2] = (int64_t)e.support.size();
+  counts[3] = (int64_t)e.inlets.size();
+  return lbgpu_get_tables(&e, tag, bc_T, bc_axis, bc_sign, w, mask, design, support, A);
+}
+
+void lbgpu_destroy(lbgpu_engine* e) { delete e; }
+const char* lbgpu_last_create_error(void) { return g_create_err.c_str(); }
+const char* lbgpu_error_message(const lbgpu_engine* e) { return e ? e->err.c_str() : "null handle"; }
+
+int lbgpu_info(const lbgpu_engine* e, int* dims, int64_t* counts) {
+  if (!e || !dims || !counts) return LBGPU_E_ARG;
+  const int d[8] = {e->nx, e->ny, e->nz, e->m, e->mf, e->mt, e->prec, e->exact};
+  std::memcpy(dims, d, sizeof d);
+  counts[0] = e->N;
+  counts[1] = (int64_t)e->design.size();
+  counts[2] = (int64_t)e->support.size();
+  counts[3] = (int64_t)e->inlets.size();
+  return LBGPU_OK;
+}
+
+int lbgpu_get_tables(const lbgpu_engine* e, uint8_t* tag, double* bc_T, int8_t* bc_axis,
+                     int8_t* bc_sign, double* w, uint8_t* mask, int64_t* design, int64_t* support,
+                     double* A) {
+  if (!e) return LBGPU_E_ARG;
+  const size_t n = size_t(e->N);
+  if (tag) std::memcpy(tag, e->tag.data(), n);
+  if (bc_T) std::memcpy(bc_T, e->bc_T.data(), n * sizeof(double));
+  if (bc_axis) std::memcpy(bc_axis, e->bc_axis.data(), n);
+  if (bc_sign) std::memcpy(bc_sign, e->bc_sign.data(), n);
+  if (w) std::memcpy(w, e->w.data(), n * sizeof(double));
+  if (mask) std::memcpy(mask, e->mask.data(), n);
+  if (design) for (size_t i = 0; i < e->design.size(); ++i) design[i] = e->design[i];
+  if (support) for (size_t i = 0; i < e->support.size(); ++i) support[i] = e->support[i];
+  if (A) std::memcpy(A, e->A.data(), e->A.size() * sizeof(double));
+  return LBGPU_OK;
+}
+
+int lbgpu_counters(const lbgpu_engine* e, int64_t* p, int64_t* a) {
+  if (!e || !p || !a) return LBGPU_E_ARG;
+  *p = e->primal_steps;
+  *a = e->adjoint_steps;
+  return LBGPU_OK;
+}
+
+void* lbgpu_stream(const lbgpu_engine* e) { return e ? (void*)e->st : nullptr; }
+
+int lbgpu_init_state(lbgpu_engine* e) {
+  return guarded(e, [&] {
+    e->init_state();
+    e->sync();
+  });
+}
+
+int lbgpu_reset_adjoint(lbgpu_engine* e) {
+  return guarded(e, [&] {
+    CU(cudaMemsetAsync(e->v[e->vc], 0, e->field_bytes(), e->st));
+    e->sync();
+  });
+}
+
+int lbgpu_upload_state(lbgpu_engine* e, int field, const double* ref) {
+  if (!ref || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->ensure_ref();
+    CU(cudaMemcpyAsync(e->d_ref, ref, sizeof(double) * e->m * e->N, cudaMemcpyHostToDevice, e->st));
+    e->from_ref(field, e->d_ref);
+    e->sync();
+  });
+}
+
+int lbgpu_download_state(lbgpu_engine* e, int field, double* ref) {
+  if (!ref || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->ensure_ref();
+    e->to_ref(field, e->d_ref);
+    CU(cudaMemcpyAsync(ref, e->d_ref, sizeof(double) * e->m * e->N, cudaMemcpyDeviceToHost, e->st));
+    e->sync();
+  });
+}
+
+int lbgpu_upload_state_device(lbgpu_engine* e, int field, const double* d_ref) {
+  if (!d_ref || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->from_ref(field, d_ref);
+    e->sync();
+  });
+}
+
+int lbgpu_download_state_device(lbgpu_engine* e, int field, double* d_ref) {
+  if (!d_ref || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->to_ref(field, d_ref);
+    e->sync();
+  });
+}
+
+int lbgpu_set_design(lbgpu_engine* e, const double* w_full) {
+  if (!w_full) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->w.assign(w_full, w_full + e->N);
+    e->build_codes();
+    CU(cudaMemcpyAsync(e->d_w, e->w.data(), sizeof(double) * e->N, cudaMemcpyHostToDevice, e->st));
+    CU(cudaMemcpyAsync(e->d_code, e->code.data(), e->N, cudaMemcpyHostToDevice, e->st));
+    e->sync();
+    if (e->exact) e->refresh_pow_tables();
+  });
+}
+
+int lbgpu_get_design(const lbgpu_engine* e, double* w_full) {
+  if (!e || !w_full) return LBGPU_E_ARG;
+  std::memcpy(w_full, e->w.data(), sizeof(double) * e->N);
+  return LBGPU_OK;
+}
+
+int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual) {
+  return guarded(e, [&] {
+    const double r = e->steps(0, n, 0, residual != nullptr);
+    if (residual) *residual = r;
+  });
+}
+
+int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual) {
+  if (kernel != 0 && kernel != 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    const double r = e->steps(1, n, kernel, residual != nullptr);
+    if (residual) *residual = r;
+  });
+}
+
+int lbgpu_solve_primal(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed,
+                       int64_t* iters, double* residual, int* converged) {
+  if (!iters || !residual || !converged) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long it = 0;
+    e->solve(0, tol, max_iter, fixed, 0, &it, residual, converged);
+    *iters = it;
+  });
+}
+
+int lbgpu_solve_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed, int kernel,
+                        int64_t* iters, double* residual, int* converged) {
+  if (!iters || !residual || !converged || (kernel != 0 && kernel != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long it = 0;
+    e->solve(1, tol, max_iter, fixed, kernel, &it, residual, converged);
+    *iters = it;
+  });
+}
+
+int lbgpu_param_gradient(lbgpu_engine* e, int kernel, double* g, double* gdp) {
+  if (kernel != 0 && kernel != 1) return LBGPU_E_ARG;
+  return guarded(e, [&] { e->gradient(kernel, g, gdp); });
+}
+
+int lbgpu_objective(lbgpu_engine* e, double* value) {
+  if (!value) return LBGPU_E_ARG;
+  return guarded(e, [&] { *value = e->objective(); });
+}
+
+int lbgpu_penalty(lbgpu_engine* e, double* value) {
+  if (!value) return LBGPU_E_ARG;
+  return guarded(e, [&] { *value = e->penalty(); });
+}
+
+int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta, const double* lambda,
+                   int64_t record_interval, lbgpu_run_row* rows, int64_t cap, int64_t* n_rows) {
+  if (!zeta || !lambda || !n_rows || record_interval < 1 || iterations < 0) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long nr = 0;
+    e->one_shot(iterations, zeta, lambda, record_interval, rows, cap, &nr);
+    *n_rows = nr;
+  });
+}
+
+int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
+  if (!ms || steps < 0) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->reset_flags();
+    e->sync();
+    CU(cudaEventRecord(e->ev0, e->st));
+    for (int64_t k = 0; k < steps; ++k) {
+      if (which == 0) e->primal_launch(false, nullptr);
+      else e->adjoint_launch(0, false, nullptr);
+    }
+    CU(cudaEventRecord(e->ev1, e->st));
+    CU(cudaGetLastError());
+    CU(cudaEventSynchronize(e->ev1));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, e->ev0, e->ev1));
+    *ms = t;
+    e->check_bad(which == 0 ? "iteration" : "adjoint iteration");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,812 @@
+// Device kernels of the hot path. This header is compiled twice:
+//   kernels_fast.cu  (LBGPU_EXACT=0, FMA contraction on): the product path —
+//       pull-scheme sweeps with the algebraically reduced collision
+//       (rank-r MRT, moment-form adjoint, hand-derived pressure-face VJP);
+//   kernels_exact.cu (LBGPU_EXACT=1, -fmad=false): the reference-order
+//       formulation of physics.cuh everywhere (dense A, dual-number face
+//       VJP), bit-for-bit equal to the reference on identical inputs.
+//
+// Storage: SoA planes, plane p at p*N, node index x + nx*(y + ny*z) — the
+// reference layout (lattice.hpp:54-100) — but the buffers hold
+// POST-collision values (pull scheme). The reference's pre-collision state is
+// f_p(x) = post_p(x - e_p) for the primal and v_p(x) = post_p(x + e_p) for the
+// adjoint (which streams against the links, adjoint.cpp:239-249); k_to_ref /
+// k_from_ref convert. Streaming is a permutation, so the max-norm step
+// residual of the post-collision buffers equals the reference's
+// step_residual (collision.cpp:365-375) exactly.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "types.cuh"
+
+#ifndef LBGPU_EXACT
+#error "define LBGPU_EXACT"
+#endif
+#if LBGPU_EXACT
+#define LBGPU_NS exact
+#else
+#define LBGPU_NS fast
+#endif
+
+namespace lbgpu {
+
+namespace detail {
+
+LBGPU_HD long long gflat(const Geom& g, int x, int y, int z) {
+  return (long long)(x + g.gx_off) + (long long)g.gnx * (y + (long long)g.gny * z);
+}
+
+// Neighbour coordinate tables with periodic wrap on every axis of the local
+// array (primal_step's modular wrap, collision.cpp:343-351). Slab runs never
+// wrap in x because their computed columns exclude the ghost columns.
+struct Nbr {
+  int xs[3];
+  long long ys[3], zs[3];
+};
+__device__ __forceinline__ Nbr make_nbr(const Geom& g, int x, int y, int z) {
+  Nbr n;
+  n.xs[0] = x == 0 ? g.nx - 1 : x - 1;
+  n.xs[1] = x;
+  n.xs[2] = x == g.nx - 1 ? 0 : x + 1;
+  const int ym = y == 0 ? g.ny - 1 : y - 1, yp = y == g.ny - 1 ? 0 : y + 1;
+  const int zm = z == 0 ? g.nz - 1 : z - 1, zp = z == g.nz - 1 ? 0 : z + 1;
+  n.ys[0] = (long long)g.nx * ym;
+  n.ys[1] = (long long)g.nx * y;
+  n.ys[2] = (long long)g.nx * yp;
+  const long long pl = (long long)g.nx * g.ny;
+  n.zs[0] = pl * zm;
+  n.zs[1] = pl * z;
+  n.zs[2] = pl * zp;
+  return n;
+}
+// Node index of x + D*e_P (D = -1: primal pull source, +1: adjoint pull source).
+template <class L, int P, int D>
+__device__ __forceinline__ long long nbr_idx(const Nbr& n) {
+  constexpr int ex = D * cvel<L>(P, 0), ey = D * cvel<L>(P, 1), ez = D * cvel<L>(P, 2);
+  return n.xs[1 + ex] + n.ys[1 + ey] + n.zs[1 + ez];
+}
+
+template <class L, class R, int D>
+__device__ __forceinline__ void gather(const R* __restrict__ buf, long long N, const Nbr& n,
+                                       R* out) {
+  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(buf + P * N + nbr_idx<L, P, D>(n)); });
+}
+
+__device__ __forceinline__ unsigned long long absdiff_bits(double a, double b) {
+  return (unsigned long long)__double_as_longlong(fabs(a - b));
+}
+
+// Block-wide max of a bit pattern, one atomicMax per block.
+__device__ __forceinline__ void block_max_bits(unsigned long long v, unsigned long long* dst) {
+  __shared__ unsigned long long red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = (blockDim.x * blockDim.y + 31) >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nwarp ? red[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = u > v ? u : v;
+    }
+    if (lane == 0 && v) atomicMax(dst, v);
+  }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ PowPair node_pp(const Model& M, const NodeTables& t, long long idx,
+                                           uint8_t code, double w) {
+  if (!(code & CODE_HAS_W)) return t.pp_one;
+  if constexpr (EXACT) {
+    (void)M;
+    (void)w;
+    return {t.p0[idx], t.p1[idx]};
+  } else {
+    return pow_pair(M, w);
+  }
+}
+
+__device__ __forceinline__ int code_axis(uint8_t c) { return (c >> CODE_AXIS_SHIFT) & 3; }
+__device__ __forceinline__ int code_sign(uint8_t c) { return (c & CODE_NEG) ? -1 : 1; }
+
+// ---------------------------------------------------------------------
+// Fast interior collision: f' = feq(rho, G u) + A (f - feq(rho, u)) with A
+// applied in moment space, A = sum_i c_i U_i^T U_i over the relaxing rows
+// (U has orthogonal rows, so U^-1 = U^T diag(1/|U_i|^2)); the conserved rows
+// drop out at compile time, and with omega_nonhydro = 1 only the shear rows
+// remain (rank 2 in 2D, 5 in 3D). BGK is A = (1 - omega) I.
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_collide(const Model& M, PowPair pp, double omt,
+                                             const R* fin, R* out) {
+  R rho = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
+  LBGPU_FOR(J, 0, L::MF, {
+    rho += fin[J];
+    if constexpr (L::ef(J, 0) != 0) j0 = L::ef(J, 0) > 0 ? j0 + fin[J] : j0 - fin[J];
+    if constexpr (L::ef(J, 1) != 0) j1 = L::ef(J, 1) > 0 ? j1 + fin[J] : j1 - fin[J];
+    if constexpr (L::ef(J, 2) != 0) j2 = L::ef(J, 2) > 0 ? j2 + fin[J] : j2 - fin[J];
+  });
+  if (!(rho > R(0))) return false;
+  const R inv = R(1) / rho;
+  const R u[3] = {j0 * inv, j1 * inv, j2 * inv};
+  const R G = M.fluid_power ? R(pp.p0) : R(1.0 - pp.p0);
+  const R up[3] = {G * u[0], G * u[1], G * u[2]};
+  const R a0 = R(1) - R(1.5) * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  const R b0 = R(1) - R(1.5) * (up[0] * up[0] + up[1] * up[1] + up[2] * up[2]);
+  R df[L::MF];
+  LBGPU_FOR(J, 0, L::MF, {
+    const R eu = edotp<L, R, J>(u), eup = edotp<L, R, J>(up);
+    const R wr = R(L::wf(J)) * rho;
+    df[J] = fin[J] - wr * (a0 + eu * (R(3) + R(4.5) * eu));
+    out[J] = wr * (b0 + eup * (R(3) + R(4.5) * eup));
+  });
+  if constexpr (CK == 0) {
+    const R c = R(1.0 - M.om);
+#pragma unroll
+    for (int j = 0; j < L::MF; ++j) out[j] += c * df[j];
+  } else {
+    LBGPU_FOR(I, 0, L::MF, {
+      if constexpr (L::row_class(I) == 1 || (CK == 2 && L::row_class(I) == 2)) {
+        R m = R(0);
+        LBGPU_FOR(J, 0, L::MF, {
+          constexpr double uij = L::U(I, J);
+          if constexpr (uij != 0.0) m += R(uij) * df[J];
+        });
+        m *= R(M.mrt_c[I]);
+        LBGPU_FOR(J, 0, L::MF, {
+          constexpr double uij = L::U(I, J);
+          if constexpr (uij != 0.0) out[J] += R(uij) * m;
+        });
+      }
+    });
+  }
+  const R* g = fin + L::MF;
+  R T = R(0);
+#pragma unroll
+  for (int j = 0; j < L::MT; ++j) T += g[j];
+  const R om = R(omt);
+  LBGPU_FOR(J, 0, L::MT, {
+    const R eup = edotp<L, R, L::MF + J>(up);
+    const R geq = R(L::wt(J)) * T * (R(1) + R(3) * eup);
+    out[L::MF + J] = g[J] + om * (geq - g[J]);
+  });
+  return true;
+}
+
+// Thermal relaxation rate of a node (collision.cpp:210-211).
+template <class R>
+__device__ __forceinline__ double node_omt(const Model& M, const NodeTables& t, uint8_t code,
+                                           double w) {
+  if (!(code & CODE_HAS_W)) return t.omt_one;
+  const R wr = R(w);
+  const R beta = wr * R(M.beta_f) + (R(1) - wr) * R(M.beta_s);
+  return double(R(1) / (R(0.5) + R(3) * beta));
+}
+
+// Fast transpose of the interior collision Jacobian (interior_vjp,
+// adjoint.cpp:50-121) in moment form: every contraction with d feq/d(rho,u)
+// is accumulated directly from w_j x_j, e_j . u and e_j . G u, and A^T = A
+// (symmetric for an orthogonal moment basis) is applied like the primal.
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_vjp(const Model& M, PowPair pp, double omt, const R* f,
+                                         const R* g, const R* vf, const R* vg, R* outf, R* outg) {
+  R rho = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
+  LBGPU_FOR(J, 0, L::MF, {
+    rho += f[J];
+    if constexpr (L::ef(J, 0) != 0) j0 = L::ef(J, 0) > 0 ? j0 + f[J] : j0 - f[J];
+    if constexpr (L::ef(J, 1) != 0) j1 = L::ef(J, 1) > 0 ? j1 + f[J] : j1 - f[J];
+    if constexpr (L::ef(J, 2) != 0) j2 = L::ef(J, 2) > 0 ? j2 + f[J] : j2 - f[J];
+  });
+  if (!(rho > R(0))) return false;
+  const R inv = R(1) / rho;
+  const R u[3] = {j0 * inv, j1 * inv, j2 * inv};
+  const R G = M.fluid_power ? R(pp.p0) : R(1.0 - pp.p0);
+  const R up[3] = {G * u[0], G * u[1], G * u[2]};
+  const R a0 = R(1) - R(1.5) * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  const R b0 = R(1) - R(1.5) * (up[0] * up[0] + up[1] * up[1] + up[2] * up[2]);
+
+  // r = A^T vf
+  R* r = outf;  // r lives in the output registers until the final update
+  if constexpr (CK == 0) {
+    const R c = R(1.0 - M.om);
+#pragma unroll
+    for (int j = 0; j < L::MF; ++j) r[j] = c * vf[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < L::MF; ++j) r[j] = R(0);
+    LBGPU_FOR(I, 0, L::MF, {
+      if constexpr (L::row_class(I) == 1 || (CK == 2 && L::row_class(I) == 2)) {
+        R m = R(0);
+        LBGPU_FOR(J, 0, L::MF, {
+          constexpr double uij = L::U(I, J);
+          if constexpr (uij != 0.0) m += R(uij) * vf[J];
+        });
+        m *= R(M.mrt_c[I]);
+        LBGPU_FOR(J, 0, L::MF, {
+          constexpr double uij = L::U(I, J);
+          if constexpr (uij != 0.0) r[J] += R(uij) * m;
+        });
+      }
+    });
+  }
+
+  R Pr = R(0), Rr = R(0), P0 = R(0), R0 = R(0);
+  R Pu[3] = {R(0), R(0), R(0)}, Ru[3] = {R(0), R(0), R(0)};
+  LBGPU_FOR(J, 0, L::MF, {
+    const R eu = edotp<L, R, J>(u), eup = edotp<L, R, J>(up);
+    const R tv = R(L::wf(J)) * vf[J];
+    const R tr = R(L::wf(J)) * r[J];
+    Pr += tv * (b0 + eup * (R(3) + R(4.5) * eup));
+    Rr += tr * (a0 + eu * (R(3) + R(4.5) * eu));
+    P0 += tv;
+    R0 += tr;
+    const R sp = tv * (R(3) + R(9) * eup);
+    const R sr = tr * (R(3) + R(9) * eu);
+    if constexpr (L::ef(J, 0) != 0) { Pu[0] += L::ef(J, 0) > 0 ? sp : -sp; Ru[0] += L::ef(J, 0) > 0 ? sr : -sr; }
+    if constexpr (L::ef(J, 1) != 0) { Pu[1] += L::ef(J, 1) > 0 ? sp : -sp; Ru[1] += L::ef(J, 1) > 0 ? sr : -sr; }
+    if constexpr (L::ef(J, 2) != 0) { Pu[2] += L::ef(J, 2) > 0 ? sp : -sp; Ru[2] += L::ef(J, 2) > 0 ? sr : -sr; }
+  });
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    Pu[a] = rho * (Pu[a] - R(3) * up[a] * P0);
+    Ru[a] = rho * (Ru[a] - R(3) * u[a] * R0);
+  }
+
+  R T = R(0), St0 = R(0), St1[3] = {R(0), R(0), R(0)};
+  LBGPU_FOR(J, 0, L::MT, {
+    T += g[J];
+    const R tw = R(L::wt(J)) * vg[J];
+    St0 += tw;
+    if constexpr (L::et(J, 0) != 0) St1[0] += L::et(J, 0) > 0 ? tw : -tw;
+    if constexpr (L::et(J, 1) != 0) St1[1] += L::et(J, 1) > 0 ? tw : -tw;
+    if constexpr (L::et(J, 2) != 0) St1[2] += L::et(J, 2) > 0 ? tw : -tw;
+  });
+  const R om = R(omt);
+  const R sigma = St0 + R(3) * (up[0] * St1[0] + up[1] * St1[1] + up[2] * St1[2]);
+  const R s3 = R(3) * om * T;
+  R c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) c[a] = G * (Pu[a] + s3 * St1[a]) - Ru[a];
+  const R s0 = Pr - Rr - (c[0] * u[0] + c[1] * u[1] + c[2] * u[2]) * inv;
+  const R ci[3] = {c[0] * inv, c[1] * inv, c[2] * inv};
+  LBGPU_FOR(K_, 0, L::MF, { outf[K_] = r[K_] + s0 + edotp<L, R, K_>(ci); });
+  const R om1 = R(1) - om, oms = om * sigma;
+#pragma unroll
+  for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k] + oms;
+  return true;
+}
+
+// Fast pressure-face adjoint: v_out = J_recon^T (J_int(frec, grec)^T v), the
+// chain rule through collide_node's wet-node treatment (collision.cpp:248-292)
+// with the Zou-He / thermal reconstruction reversed by hand. Follows the
+// branch the primal value takes at the u_clamp test, like the reference's
+// dual sweep (dual.hpp:12-13).
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_face_vjp(const Model& M, PowPair pp, double omt, int tag,
+                                              int axis, int sign, double bcT, const R* fin,
+                                              const R* vin, R* vout) {
+  const R* f = fin;
+  const R* g = fin + L::MF;
+  R frec[L::MF], grec[L::MT];
+  const R rho_t = R(tag == TAG_INLET ? M.rho_in : M.rho_out);
+  face_recon<L, R>(M, tag, axis, sign, bcT, fin, rho_t, frec, grec);
+
+  // Scalars of the forward reconstruction.
+  R k0 = R(0), km = R(0);
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) {
+    const int ea = evel_axis(L::ef(j, 0), L::ef(j, 1), L::ef(j, 2), axis);
+    if (ea == 0) k0 += f[j];
+    else if (ea == -sign) km += f[j];
+  }
+  const R s = R(sign);
+  const R Ksum = k0 + R(2) * km;
+  R ua = s * (R(1) - Ksum / rho_t);
+  R rho = rho_t;
+  const bool clamped = (ua < R(0) ? -ua : ua) > R(M.u_clamp);
+  if (clamped) {
+    ua = ua > R(0) ? R(M.u_clamp) : R(-M.u_clamp);
+    rho = Ksum / (R(1) - s * ua);
+  }
+  R Tstar = R(bcT), tden = R(1);
+  if (tag == TAG_OUTLET) {
+    R tnum = R(0);
+    tden = R(0);
+#pragma unroll
+    for (int j = 0; j < L::MT; ++j) {
+      const int ea = evel_axis(L::et(j, 0), L::et(j, 1), L::et(j, 2), axis);
+      if (ea == sign) continue;
+      tnum += g[j];
+      tden += R(L::wt(j)) * (R(1) + R(3) * (R(ea) * ua));
+    }
+    Tstar = tnum / tden;
+  }
+
+  R af[L::MF], ag[L::MT];
+  if (!fast_vjp<L, R, CK>(M, pp, omt, frec, grec, vin, vin + L::MF, af, ag)) return false;
+
+  R* of = vout;
+  R* og = vout + L::MF;
+  R afeq[L::MF];
+  R anb[3] = {R(0), R(0), R(0)};
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) of[j] = R(0), afeq[j] = R(0);
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) {
+    const int e[3] = {L::ef(j, 0), L::ef(j, 1), L::ef(j, 2)};
+    if (e[axis] != sign) {
+      of[j] += af[j];
+    } else {
+      const int o = L::oppf(j);
+      of[o] += af[j];
+      afeq[j] += af[j];
+      afeq[o] -= af[j];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != axis && e[b]) anb[b] -= af[j] * R(e[b]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) {
+    const int e[3] = {L::ef(j, 0), L::ef(j, 1), L::ef(j, 2)};
+    if (e[axis] != 0) continue;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      if (b != axis && e[b]) of[j] += R(0.5 * e[b]) * anb[b];
+  }
+  R arho = R(0), aua = R(0);
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) {
+    const R ea = R(evel_axis(L::ef(j, 0), L::ef(j, 1), L::ef(j, 2), axis));
+    const R wj = R(L::wf(j));
+    const R eu = ea * ua;
+    arho += afeq[j] * wj * (R(1) + R(3) * eu + R(4.5) * eu * eu - R(1.5) * ua * ua);
+    aua += afeq[j] * wj * rho * (R(3) * ea + R(9) * ea * eu - R(3) * ua);
+  }
+  R aT = R(0);
+#pragma unroll
+  for (int j = 0; j < L::MT; ++j) {
+    const R ea = R(evel_axis(L::et(j, 0), L::et(j, 1), L::et(j, 2), axis));
+    const R tw = R(L::wt(j));
+    aT += ag[j] * tw * (R(1) + R(3) * ea * ua);
+    aua += ag[j] * tw * Tstar * R(3) * ea;
+    og[j] = R(0);
+  }
+  if (tag == TAG_OUTLET) {
+    const R atnum = aT / tden;
+    const R atden = -aT * Tstar / tden;
+#pragma unroll
+    for (int j = 0; j < L::MT; ++j) {
+      const int ea = evel_axis(L::et(j, 0), L::et(j, 1), L::et(j, 2), axis);
+      if (ea == sign) continue;
+      og[j] += atnum;
+      aua += atden * R(L::wt(j)) * R(3) * R(ea);
+    }
+  }
+  const R aK = clamped ? arho / (R(1) - s * ua) : -aua * s / rho_t;
+#pragma unroll
+  for (int j = 0; j < L::MF; ++j) {
+    const int ea = evel_axis(L::ef(j, 0), L::ef(j, 1), L::ef(j, 2), axis);
+    if (ea == 0) of[j] += aK;
+    else if (ea == -sign) of[j] += R(2) * aK;
+  }
+  return true;
+}
+
+}  // namespace detail
+
+// ====================================================================
+// Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
+
+// Primal sweep (primal_step, collision.cpp:308-363, in pull form) with the
+// node dispatch of collide_node (collision.cpp:219-294), the rho <= 0 flag
+// (collision.hpp:103) and, when RESID, the fused step_residual.
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
+                                                R* __restrict__ dst) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  unsigned long long rmax = 0;
+  if (x < g.x1) {
+    const long long N = g.N;
+    const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+    const Nbr nb = make_nbr(g, x, y, z);
+    R f[L::M];
+    gather<L, R, -1>(src, N, nb, f);
+    const uint8_t code = a.t.code[idx];
+    const int tag = code & TAG_MASK;
+    R out[L::M];
+    bool ok = true;
+    if (tag == TAG_WALL) {
+      LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
+    } else if (tag == TAG_HEATER) {
+      LBGPU_FOR(P, 0, L::MF, { out[P] = f[L::oppf(P)]; });
+      const R T = R(a.t.bcT[idx]);
+#pragma unroll
+      for (int j = 0; j < L::MT; ++j) out[L::MF + j] = R(L::wt(j)) * T * (R(1) + R(3) * R(0));
+    } else {
+      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+#if LBGPU_EXACT
+      ok = collide_node<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f,
+                              R(w), R(a.M.rho_in), out);
+#else
+      const double omt = node_omt<R>(a.M, a.t, code, w);
+      if (tag == TAG_INTERIOR) {
+        ok = fast_collide<L, R, CK>(a.M, pp, omt, f, out);
+      } else {
+        R rec[L::M];
+        face_recon<L, R>(a.M, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f,
+                         R(a.M.rho_in), rec, rec + L::MF);
+        ok = fast_collide<L, R, CK>(a.M, pp, omt, rec, out);
+      }
+#endif
+    }
+    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = out[P]; });
+    if constexpr (RESID) {
+      LBGPU_FOR(P, 0, L::M, {
+        constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
+        const R old = rest ? f[P] : __ldg(src + P * N + idx);
+        const unsigned long long d = absdiff_bits(double(out[P]), double(old));
+        rmax = d > rmax ? d : rmax;
+      });
+    }
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+}
+
+// Adjoint sweep (adjoint_step, adjoint.cpp:206-254, in pull form): gathers v
+// against the links and the frozen base f along them, applies
+// adjoint_collide_node (adjoint.cpp:156-204) and stores the post-collision
+// adjoint. AK = 0 analytic kernel, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18).
+template <class L, class R, int CK, int AK, bool RESID>
+__global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__ base,
+                                                 const R* __restrict__ src,
+                                                 R* __restrict__ dst) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  unsigned long long rmax = 0;
+  if (x < g.x1) {
+    const long long N = g.N;
+    const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+    const Nbr nb = make_nbr(g, x, y, z);
+    R vin[L::M];
+    gather<L, R, +1>(src, N, nb, vin);
+    const uint8_t code = a.t.code[idx];
+    const int tag = code & TAG_MASK;
+    R vout[L::M];
+    bool ok = true;
+    R fin[L::M];
+    const bool need_base = AK == 1 || !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
+    if (need_base) gather<L, R, -1>(base, N, nb, fin);
+    if (AK == 0 && tag == TAG_WALL) {
+      LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+    } else if (AK == 0 && tag == TAG_HEATER) {
+      LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+#pragma unroll
+      for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
+    } else {
+      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+      if (AK == 1 || (LBGPU_EXACT && tag != TAG_INTERIOR)) {
+        ok = vjp_dual<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], fin,
+                            R(w), vin, vout);
+      } else {
+#if LBGPU_EXACT
+        ok = interior_vjp<L, R>(a.M, pp, fin, fin + L::MF, R(w), vin, vin + L::MF, vout,
+                                vout + L::MF);
+#else
+        const double omt = node_omt<R>(a.M, a.t, code, w);
+        if (tag == TAG_INTERIOR)
+          ok = fast_vjp<L, R, CK>(a.M, pp, omt, fin, fin + L::MF, vin, vin + L::MF, vout,
+                                  vout + L::MF);
+        else
+          ok = fast_face_vjp<L, R, CK>(a.M, pp, omt, tag, code_axis(code), code_sign(code),
+                                       a.t.bcT[idx], fin, vin, vout);
+#endif
+      }
+    }
+    if (code & CODE_SUPPORT) {
+      R b[L::M];
+      if (node_partial<L, R>(a.M, fin, b)) {
+#pragma unroll
+        for (int p = 0; p < L::M; ++p) vout[p] += b[p];
+      } else {
+        ok = false;
+      }
+    }
+    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = vout[P]; });
+    if constexpr (RESID) {
+      LBGPU_FOR(P, 0, L::M, {
+        constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
+        const R old = rest ? vin[P] : __ldg(src + P * N + idx);
+        const unsigned long long d = absdiff_bits(double(vout[P]), double(old));
+        rmax = d > rmax ? d : rmax;
+      });
+    }
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+}
+
+// Per-design-node gradient (param_gradient's design part, adjoint.cpp:377-398)
+// with, when UPDATE, the one-shot composite/ascent step fused in
+// (optimizer.cpp:41-45, descent_update :8-16). The node list holds local
+// indices in ascending global order.
+template <class L, class R, int AK, bool UPDATE>
+__global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict__ p,
+                                                  const R* __restrict__ q,
+                                                  const long long* __restrict__ nodes,
+                                                  long long n, double* __restrict__ gout,
+                                                  double* __restrict__ w_rw, double zeta,
+                                                  double lambda) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long cmax = 0;
+  if (i < n) {
+    const Geom& g = a.g;
+    const long long idx = nodes[i];
+    const int x = int(idx % g.nx);
+    const int y = int((idx / g.nx) % g.ny);
+    const int z = int(idx / ((long long)g.nx * g.ny));
+    const Nbr nb = make_nbr(g, x, y, z);
+    R f[L::M], v[L::M];
+    gather<L, R, -1>(p, g.N, nb, f);
+    gather<L, R, +1>(q, g.N, nb, v);
+    const uint8_t code = a.t.code[idx];
+    const double w = a.t.w[idx];
+    const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
+    double gv = 0.0;
+    bool ok;
+    if (AK == 0 && (code & TAG_MASK) == TAG_INTERIOR) {
+      ok = design_gradient<L, R>(a.M, pp, f, f + L::MF, R(w), v, v + L::MF, gv);
+    } else {  // design_gradient_node_dual (adjoint.cpp:361-373)
+      Dual<R> din[L::M], dout[L::M];
+#pragma unroll
+      for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(f[k]);
+      ok = collide_node<L>(a.M, pp, code & TAG_MASK, code_axis(code), code_sign(code),
+                           a.t.bcT[idx], din, Dual<R>(R(w), R(1)), Dual<R>(R(a.M.rho_in)), dout);
+      R acc = R(0);
+#pragma unroll
+      for (int k = 0; k < L::M; ++k) acc = acc + v[k] * dout[k].d;
+      gv = double(acc);
+    }
+    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    if constexpr (UPDATE) {
+      double comp = gv;
+      if (lambda != 0.0) comp -= lambda * (1.0 - 2.0 * w);
+      double wn = w + zeta * comp;
+      wn = wn < 0.0 ? 0.0 : (1.0 < wn ? 1.0 : wn);
+      w_rw[idx] = wn;
+      cmax = (unsigned long long)__double_as_longlong(fabs(comp));
+    } else {
+      gout[i] = gv;
+    }
+  }
+  if constexpr (UPDATE) block_max_bits(cmax, a.fl.aux);
+}
+
+// Objective terms F^x on the support list (evaluate_raw, objective.cpp:64-72).
+template <class L, class R>
+__global__ void k_objective_terms(Launch a, const R* __restrict__ p,
+                                  const long long* __restrict__ nodes, long long n,
+                                  double* __restrict__ terms) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Geom& g = a.g;
+  const long long idx = nodes[i];
+  const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
+  const Nbr nb = make_nbr(g, x, y, z);
+  R f[L::M];
+  gather<L, R, -1>(p, g.N, nb, f);
+  R t;
+  if (!node_term<L, R>(a.M, f, t)) {
+    atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    t = R(NAN);
+  }
+  terms[i] = double(t);
+}
+
+// Inlet-overpressure global (param_gradient, adjoint.cpp:399-418): one dual
+// collision per inlet node with rho_target seeded by 3.
+template <class L, class R>
+__global__ void k_inlet_terms(Launch a, const R* __restrict__ p, const R* __restrict__ q,
+                              const long long* __restrict__ nodes, long long n,
+                              double* __restrict__ terms) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Geom& g = a.g;
+  const long long idx = nodes[i];
+  const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
+  const Nbr nb = make_nbr(g, x, y, z);
+  R f[L::M], v[L::M];
+  gather<L, R, -1>(p, g.N, nb, f);
+  gather<L, R, +1>(q, g.N, nb, v);
+  const uint8_t code = a.t.code[idx];
+  const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+  const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+  Dual<R> din[L::M], dout[L::M];
+#pragma unroll
+  for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(f[k]);
+  const bool ok = collide_node<L>(a.M, pp, code & TAG_MASK, code_axis(code), code_sign(code),
+                                  a.t.bcT[idx], din, Dual<R>(R(w)),
+                                  Dual<R>(R(a.M.rho_in), R(3)), dout);
+  if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+  R acc = R(0);
+#pragma unroll
+  for (int k = 0; k < L::M; ++k) acc = acc + v[k] * dout[k].d;
+  terms[i] = double(acc);
+}
+
+// Reference-layout conversion. D = -1: primal (f_ref(x) = post(x - e)),
+// D = +1: adjoint (v_ref(x) = post(x + e)). TO_REF gathers post -> ref,
+// otherwise scatters ref -> post (the exact inverse permutation).
+template <class L, class R, int D, bool TO_REF>
+__global__ void k_layout(Geom g, const void* __restrict__ in, void* __restrict__ out) {
+  using namespace detail;
+  const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.x1) return;
+  const long long N = g.N;
+  const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+  const Nbr nb = make_nbr(g, x, y, z);
+  if constexpr (TO_REF) {
+    const R* post = static_cast<const R*>(in);
+    double* ref = static_cast<double*>(out);
+    LBGPU_FOR(P, 0, L::M, { ref[P * N + idx] = double(post[P * N + nbr_idx<L, P, D>(nb)]); });
+  } else {
+    const double* ref = static_cast<const double*>(in);
+    R* post = static_cast<R*>(out);
+    // post(y) = ref(y - D e)
+    LBGPU_FOR(P, 0, L::M, { post[P * N + idx] = R(ref[P * N + nbr_idx<L, P, -D>(nb)]); });
+  }
+}
+
+// initialize_state (collision.cpp:296-306): flow planes at w_j, thermal 0.
+// Uniform planes are invariant under streaming, so the post-collision layout
+// holds the same values.
+template <class L, class R>
+__global__ void k_init(long long N, R* __restrict__ buf) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+#pragma unroll
+  for (int p = 0; p < L::M; ++p) buf[p * N + i] = p < L::MF ? R(L::wf(p)) : R(0);
+}
+
+// ---------------------------------------------------------------------
+// Host-side launchers (one set per build), dispatched by the engine.
+namespace LBGPU_NS {
+
+
+template <class L, class R, int CK, bool RES>
+void primal_t(const SweepArgs& s, const void* src, void* dst) {
+  const Geom& g = s.a.g;
+  const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
+  dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
+  k_primal<L, R, CK, RES><<<grid, bx, 0, s.a.stream>>>(s.a, static_cast<const R*>(src),
+                                                        static_cast<R*>(dst));
+}
+template <class L, class R, int CK, int AK, bool RES>
+void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst) {
+  const Geom& g = s.a.g;
+  const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
+  dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
+  k_adjoint<L, R, CK, AK, RES><<<grid, bx, 0, s.a.stream>>>(
+      s.a, static_cast<const R*>(base), static_cast<const R*>(src), static_cast<R*>(dst));
+}
+
+#define LBGPU_CK_DISPATCH(...)                                        \
+  do {                                                                \
+    if (s.ck == 0) { constexpr int CKV = 0; __VA_ARGS__; }            \
+    else if (s.ck == 1) { constexpr int CKV = 1; __VA_ARGS__; }       \
+    else { constexpr int CKV = 2; __VA_ARGS__; }                      \
+  } while (0)
+
+template <class L, class R>
+void primal_l(const SweepArgs& s, const void* src, void* dst) {
+#if LBGPU_EXACT
+  if (s.resid) primal_t<L, R, 0, true>(s, src, dst);
+  else primal_t<L, R, 0, false>(s, src, dst);
+#else
+  if (s.resid) LBGPU_CK_DISPATCH((primal_t<L, R, CKV, true>(s, src, dst)));
+  else LBGPU_CK_DISPATCH((primal_t<L, R, CKV, false>(s, src, dst)));
+#endif
+}
+template <class L, class R, int AK>
+void adjoint_l(const SweepArgs& s, const void* base, const void* src, void* dst) {
+  if constexpr (AK == 1 || LBGPU_EXACT) {
+    if (s.resid) adjoint_t<L, R, 0, AK, true>(s, base, src, dst);
+    else adjoint_t<L, R, 0, AK, false>(s, base, src, dst);
+  } else {
+    if (s.resid) LBGPU_CK_DISPATCH((adjoint_t<L, R, CKV, 0, true>(s, base, src, dst)));
+    else LBGPU_CK_DISPATCH((adjoint_t<L, R, CKV, 0, false>(s, base, src, dst)));
+  }
+}
+
+#define LBGPU_LR_DISPATCH(DIM, PREC, ...)                                   \
+  do {                                                                      \
+    if ((DIM) == 2 && (PREC) == 64) { using L = LatD2; using R = double; __VA_ARGS__; } \
+    else if ((DIM) == 2) { using L = LatD2; using R = float; __VA_ARGS__; } \
+    else if ((PREC) == 64) { using L = LatD3; using R = double; __VA_ARGS__; } \
+    else { using L = LatD3; using R = float; __VA_ARGS__; }                 \
+  } while (0)
+
+#if defined(LBGPU_PART_PRIMAL)
+void primal(const SweepArgs& s, const void* src, void* dst) {
+  LBGPU_LR_DISPATCH(s.dim, s.prec, (primal_l<L, R>(s, src, dst)));
+}
+#endif
+#if defined(LBGPU_PART_ADJOINT)
+void adjoint(const SweepArgs& s, const void* base, const void* src, void* dst) {
+  LBGPU_LR_DISPATCH(s.dim, s.prec, (adjoint_l<L, R, 0>(s, base, src, dst)));
+}
+#endif
+#if defined(LBGPU_PART_ADJDUAL)
+void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* dst) {
+  LBGPU_LR_DISPATCH(s.dim, s.prec, (adjoint_l<L, R, 1>(s, base, src, dst)));
+}
+#endif
+#if defined(LBGPU_PART_AUX)
+void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,
+              const void* q, const long long* nodes, long long n, double* gout, double* w_rw,
+              double zeta, double lambda) {
+  if (n <= 0) return;
+  const int bs = 128;
+  const unsigned nb = unsigned((n + bs - 1) / bs);
+  LBGPU_LR_DISPATCH(dim, prec, {
+    const R* pp = static_cast<const R*>(p);
+    const R* qq = static_cast<const R*>(q);
+    if (ak == 0 && !update) k_gradient<L, R, 0, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
+    else if (ak == 0) k_gradient<L, R, 0, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
+    else if (!update) k_gradient<L, R, 1, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
+    else k_gradient<L, R, 1, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
+  });
+}
+void objective_terms(const Launch& a, int dim, int prec, const void* p, const long long* nodes,
+                     long long n, double* terms) {
+  if (n <= 0) return;
+  const unsigned nb = unsigned((n + 127) / 128);
+  LBGPU_LR_DISPATCH(dim, prec, (k_objective_terms<L, R><<<nb, 128, 0, a.stream>>>(
+                                    a, static_cast<const R*>(p), nodes, n, terms)));
+}
+void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,
+                 const long long* nodes, long long n, double* terms) {
+  if (n <= 0) return;
+  const unsigned nb = unsigned((n + 127) / 128);
+  LBGPU_LR_DISPATCH(dim, prec, (k_inlet_terms<L, R><<<nb, 128, 0, a.stream>>>(
+                                    a, static_cast<const R*>(p), static_cast<const R*>(q),
+                                    nodes, n, terms)));
+}
+#endif
+#if defined(LBGPU_PART_PRIMAL)
+void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in, void* out,
+            cudaStream_t st) {
+  const int bx = (g.x1 - g.x0) >= 128 ? 128 : 32;
+  dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
+  LBGPU_LR_DISPATCH(dim, prec, {
+    if (field == 0 && to_ref) k_layout<L, R, -1, true><<<grid, bx, 0, st>>>(g, in, out);
+    else if (field == 0) k_layout<L, R, -1, false><<<grid, bx, 0, st>>>(g, in, out);
+    else if (to_ref) k_layout<L, R, +1, true><<<grid, bx, 0, st>>>(g, in, out);
+    else k_layout<L, R, +1, false><<<grid, bx, 0, st>>>(g, in, out);
+  });
+}
+void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st) {
+  const unsigned nb = unsigned((N + 255) / 256);
+  LBGPU_LR_DISPATCH(dim, prec, (k_init<L, R><<<nb, 256, 0, st>>>(N, static_cast<R*>(buf))));
+}
+#endif
+
+}  // namespace LBGPU_NS
+}  // namespace lbgpu

@@ -1,0 +1,68 @@
+// Plain structs shared by the kernels and the host engine.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "physics.cuh"
+
+namespace lbgpu {
+
+struct Geom {
+  int nx, ny, nz;   // local array extents
+  int x0, x1;       // computed (owned) local columns [x0, x1)
+  long long N;      // nodes of the local array = plane stride
+  int gx_off;       // global x = local x + gx_off
+  int gnx, gny;     // global extents (flat index for error reports)
+};
+
+struct NodeTables {
+  const uint8_t* code;
+  const double* w;
+  const double* bcT;
+  const double* p0;  // exact build: host-glibc pow(base, theta) per node
+  const double* p1;  //              pow(base, theta - 1)
+  PowPair pp_one;    // pow pair of non-design nodes (w == 1)
+  double omt_one;    // thermal relaxation rate at w == 1
+};
+
+struct Flags {
+  unsigned long long* resid;  // NaN-propagating max |new-old| as a bit pattern
+  unsigned long long* bad;    // smallest global flat index with rho <= 0
+  unsigned long long* aux;    // kernel-specific (max |comp| for design updates)
+  unsigned long long step_key;  // (step number << 40): orders "bad" reports by step
+};
+
+struct Launch {
+  Geom g;
+  NodeTables t;
+  Model M;
+  Flags fl;
+  cudaStream_t stream;
+};
+
+struct SweepArgs {
+  Launch a;
+  int dim, prec, ck;  // ck: 0 bgk, 1 mrt (shear rows), 2 mrt + non-hydro rows
+  bool resid;
+};
+
+// Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).
+#define LBGPU_DECLARE_LAUNCHERS(NS)                                                          \
+  namespace NS {                                                                           \
+  void primal(const SweepArgs& s, const void* src, void* dst);                             \
+  void adjoint(const SweepArgs& s, const void* base, const void* src, void* dst);          \
+  void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* dst);     \
+  void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,    \
+                const void* q, const long long* nodes, long long n, double* gout,          \
+                double* w_rw, double zeta, double lambda);                                 \
+  void objective_terms(const Launch& a, int dim, int prec, const void* p,                  \
+                       const long long* nodes, long long n, double* terms);                \
+  void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,       \
+                   const long long* nodes, long long n, double* terms);                    \
+  void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
+              void* out, cudaStream_t st);                                                 \
+  void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
+  }
+LBGPU_DECLARE_LAUNCHERS(fast)
+LBGPU_DECLARE_LAUNCHERS(exact)
+
+}  // namespace lbgpu

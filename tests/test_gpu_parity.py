@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+* exact build (``exact=True``): bit-for-bit equal to the oracle restatement
+  (itself bit-for-bit equal to the reference, tests/test_oracle.py) for
+  states, residuals, adjoint states, gradients, objectives and penalties;
+* fast build (the product path): within the tolerances SURVEY.md §8(d)
+  recommends at FP64 — per-step state and adjoint state <= 1e-12 relative to
+  max|x|, objective <= 1e-12 relative, design gradient <= 1e-10 of max|g|.
+"""
+import numpy as np
+import pytest
+
+from cases import CASES, case_text
+
+pytestmark = pytest.mark.gpu
+
+STATE_RTOL = 1e-12
+GRAD_RTOL = 1e-10
+OBJ_RTOL = 1e-12
+
+
+def rel(a, b):
+    scale = max(np.max(np.abs(b)), 1e-300)
+    return float(np.max(np.abs(a - b)) / scale)
+
+
+def make(P, O, name, exact, steps=30, asteps=20):
+    txt = case_text(name)
+    e = P.Engine.from_config(txt, exact=exact)
+    o = O.COracle(txt)
+    e.init_state()
+    o.init_state()
+    return e, o
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_exact_bitwise(lbgpu, oracle_mod, has_gpu, name):
+    e, o = make(lbgpu, oracle_mod, name, exact=True)
+    # masks and tables
+    te, to = e.tables(), o.tables()
+    for k in ("tag", "bc_T", "bc_axis", "bc_sign", "w", "mask", "design", "support", "A"):
+        assert np.array_equal(te[k], to[k]), k
+    # primal: 1, then 10 more, then 40 more steps
+    for k in (1, 10, 40):
+        re_ = e.primal_step(k)
+        ro = o.primal_steps(k)
+        assert np.array_equal(e.get_state(0), o.f), f"primal state after +{k}"
+        assert re_ == ro, (re_, ro)
+    assert e.objective() == o.objective()
+    # adjoint (analytic), against the current state
+    for k in (1, 15):
+        re_ = e.adjoint_step(k, kernel=0)
+        ro = o.adjoint_steps(k, kernel=0)
+        assert np.array_equal(e.get_state(1), o.v), f"adjoint state after +{k}"
+        assert re_ == ro
+    ge, gde = e.param_gradient(0)
+    go, gdo = o.gradient(0)
+    assert np.array_equal(ge, go)
+    assert gde == gdo
+    # dual-sweep kernel
+    re_ = e.adjoint_step(2, kernel=1)
+    ro = o.adjoint_steps(2, kernel=1)
+    assert np.array_equal(e.get_state(1), o.v)
+    ge, gde = e.param_gradient(1)
+    go, gdo = o.gradient(1)
+    assert np.array_equal(ge, go) and gde == gdo
+    assert e.penalty() == o.penalty()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fast_tolerance(lbgpu, oracle_mod, has_gpu, name):
+    e, o = make(lbgpu, oracle_mod, name, exact=False)
+    for k in (1, 50):
+        e.primal_step(k)
+        o.primal_steps(k)
+        assert rel(e.get_state(0), o.f) <= STATE_RTOL, f"primal +{k}"
+    oe, oo = e.objective(), o.objective()
+    assert abs(oe - oo) <= OBJ_RTOL * max(abs(oo), 1e-300) + 1e-18
+    for k in (1, 20):
+        e.adjoint_step(k, kernel=0)
+        o.adjoint_steps(k, kernel=0)
+        assert rel(e.get_state(1), o.v) <= STATE_RTOL, f"adjoint +{k}"
+    ge, gde = e.param_gradient(0)
+    go, gdo = o.gradient(0)
+    if go.size:
+        assert np.max(np.abs(ge - go)) <= GRAD_RTOL * max(np.max(np.abs(go)), 1e-300)
+    assert abs(gde - gdo) <= GRAD_RTOL * max(abs(gdo), 1e-300)
+    # the dual-sweep kernel in the fast build
+    e.adjoint_step(1, kernel=1)
+    o.adjoint_steps(1, kernel=1)
+    assert rel(e.get_state(1), o.v) <= STATE_RTOL
+
+
+@pytest.mark.parametrize("name", ["grad2d", "mix3d"])
+def test_layout_round_trip(lbgpu, oracle_mod, has_gpu, name):
+    """upload/download is the exact inverse permutation (both fields)."""
+    e = lbgpu.Engine.from_config(case_text(name))
+    rng = np.random.default_rng(5)
+    for field in (0, 1):
+        x = rng.standard_normal(e.m * e.n)
+        e.set_state(field, x)
+        assert np.array_equal(e.get_state(field), x)
+
+
+def test_upload_then_step_matches(lbgpu, oracle_mod, has_gpu):
+    """A state uploaded in reference layout steps exactly like the oracle."""
+    txt = case_text("mix3d")
+    e = lbgpu.Engine.from_config(txt, exact=True)
+    o = oracle_mod.COracle(txt)
+    o.init_state()
+    o.primal_steps(7)
+    e.set_state(0, o.f)
+    o.primal_steps(3)
+    e.primal_step(3)
+    assert np.array_equal(e.get_state(0), o.f)
+    rng = np.random.default_rng(1)
+    v0 = rng.uniform(-0.3, 0.3, e.m * e.n)
+    e.set_state(1, v0)
+    o.v[:] = v0
+    e.adjoint_step(2)
+    o.adjoint_steps(2)
+    assert np.array_equal(e.get_state(1), o.v)
+
+
+def test_gradcheck_preset_known_answers(lbgpu, has_gpu):
+    """gradcheck2d to 1e-12: 16,578 iterations, objective 0.0126428346367474
+    (measured with the reference)."""
+    from paper_1501_04741_b200.presets import preset_text
+    e = lbgpu.Engine.from_config(preset_text("gradcheck2d"), exact=True)
+    it, r, conv = e.solve_primal(1e-12, 200000)
+    assert (it, conv) == (16578, True)
+    assert r <= 1e-12
+    assert e.objective() == 0.012642834636747431
+    f = lbgpu.Engine.from_config(preset_text("gradcheck2d"))
+    it2, r2, conv2 = f.solve_primal(1e-12, 200000)
+    assert conv2 and abs(it2 - 16578) <= 1
+    assert abs(f.objective() - 0.012642834636747431) <= 1e-12 * 0.0127
+
+
+def test_solve_stop_iteration_matches_reference(lbgpu, oracle_mod, has_gpu):
+    """Tol-stop iteration and final residual equal the reference's exactly."""
+    txt = case_text("bgk2d")
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    r = oracle_mod.RefOracle(txt)
+    r.init_state()
+    it_r, res_r, conv_r = r.solve_primal(1e-7, 100000)
+    e = lbgpu.Engine.from_config(txt, exact=True)
+    it_e, res_e, conv_e = e.solve_primal(1e-7, 100000)
+    assert (it_e, res_e, conv_e) == (it_r, res_r, conv_r)
+    assert np.array_equal(e.get_state(0), r.get_state(0))
+    ia, ra, ca = r.solve_adjoint(1e-7, 100000)
+    ja, sa, cb = e.solve_adjoint(1e-7, 100000)
+    assert (ja, sa, cb) == (ia, ra, ca)
+    assert np.array_equal(e.get_state(1), r.get_state(1))
+    g_r, gdp_r = r.gradient()
+    g_e, gdp_e = e.param_gradient()
+    assert np.array_equal(g_e, g_r) and gdp_e == gdp_r
+
+
+def test_one_shot_exact(lbgpu, oracle_mod, has_gpu):
+    """one_shot_run: w, f, v and the record rows bit-for-bit (ζ>0, λ>0)."""
+    txt = case_text("exch2d")
+    e = lbgpu.Engine.from_config(txt, exact=True)
+    o = oracle_mod.COracle(txt)
+    e.init_state()
+    o.init_state()
+    iters = 12
+    zeta = np.full(iters, 2e-3)
+    lam = np.linspace(0.0, 0.01, iters)
+    rows = e.one_shot(zeta, lam, record_interval=5)
+    gms = [o.one_shot_iter(zeta[i], lam[i]) for i in range(iters)]
+    assert np.array_equal(e.design(), o.design())
+    assert np.array_equal(e.get_state(0), o.f)
+    assert np.array_equal(e.get_state(1), o.v)
+    assert [int(r[0]) for r in rows] == [5, 10, 12]
+    assert rows[-1][6] == gms[-1]
+    assert rows[-1][2] == o.objective()
+    assert rows[-1][3] == o.penalty()
+
+
+def test_one_shot_fast(lbgpu, oracle_mod, has_gpu):
+    txt = case_text("mix3d")
+    e = lbgpu.Engine.from_config(txt)
+    o = oracle_mod.COracle(txt)
+    e.init_state()
+    o.init_state()
+    iters = 10
+    zeta = np.full(iters, 5e-2)
+    lam = np.full(iters, 1e-3)
+    e.one_shot(zeta, lam, record_interval=10)
+    for i in range(iters):
+        o.one_shot_iter(zeta[i], lam[i])
+    assert np.max(np.abs(e.design() - o.design())) <= 1e-12
+    assert rel(e.get_state(0), o.f) <= STATE_RTOL
+    assert rel(e.get_state(1), o.v) <= 1e-11
+
+
+def test_zero_zeta_one_shot_is_plain_stepping(lbgpu, has_gpu):
+    """test_optimizer.cpp:182-209: one-shot with ζ = 0 == plain primal steps."""
+    txt = case_text("grad2d")
+    a = lbgpu.Engine.from_config(txt)
+    b = lbgpu.Engine.from_config(txt)
+    a.one_shot(np.zeros(15), np.zeros(15), record_interval=100)
+    b.primal_step(15)
+    assert np.array_equal(a.get_state(0), b.get_state(0))
+    assert np.array_equal(a.design(), b.design())
+
+
+def test_fp32_against_reference_fp32(lbgpu, oracle_mod, has_gpu):
+    """precision = 32: the GPU float path against the reference's own float
+    path at the same step counts (SURVEY.md §8d FP32 tolerances)."""
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    txt = case_text("mix3d")
+    ov = {"model.precision": 32}
+    e = lbgpu.Engine.from_config(txt, ov)
+    r = oracle_mod.RefOracle(txt, ov)
+    r.init_state()
+    e.primal_step(300)
+    r.primal_steps(300)
+    assert rel(e.get_state(0), r.get_state(0)) <= 1e-5
+    assert abs(e.objective() - r.objective()) <= 5e-4 * abs(r.objective())
+    e.adjoint_step(200)
+    r.adjoint_steps(200)
+    g_e, _ = e.param_gradient()
+    g_r, _ = r.gradient()
+    assert np.max(np.abs(g_e - g_r)) <= 1e-3 * np.max(np.abs(g_r))
+
+
+def test_nonpositive_density_reports_node(lbgpu, has_gpu):
+    """NumericError naming the first bad node (collision.cpp:355-361)."""
+    txt = case_text("periodic2d")
+    e = lbgpu.Engine.from_config(txt)
+    f = e.get_state(0)
+    nx, ny, _ = e.shape
+    n = e.n
+    # make node (3,0,0) negative in the reference layout (test_collision.cpp:288-295)
+    for j in range(e.mf):
+        f[j * n + 3] = -1.0
+    e.set_state(0, f)
+    with pytest.raises(lbgpu.LbgpuError) as ex:
+        e.primal_step(1)
+    assert ex.value.code == lbgpu.E_NUMERIC
+    assert "non-positive density at node (3,0,0)" in ex.value.msg

@@ -1,0 +1,112 @@
+"""Pins the CPU oracle: the C restatement (oracle/lbm_oracle.c) must equal
+the reference itself (oracle/_ref, compiled from /root/reference sources)
+bit for bit, on every parity case; and the committed golden fixtures
+(tests/golden/, generated from the reference by make_golden.py) must hold."""
+import os
+
+import numpy as np
+import pytest
+
+from cases import CASES, case_text
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _need_ref(O):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_restatement_equals_reference(oracle_mod, name):
+    O = oracle_mod
+    _need_ref(O)
+    txt = case_text(name)
+    c, r = O.COracle(txt), O.RefOracle(txt)
+    tc, tr = c.tables(), r.tables()
+    for k in ("tag", "bc_T", "bc_axis", "bc_sign", "w", "mask", "design", "support", "A"):
+        assert np.array_equal(tc[k], tr[k]), k
+    c.init_state()
+    r.init_state()
+    assert c.primal_steps(25) == r.primal_steps(25)
+    assert np.array_equal(c.f, r.get_state(0))
+    assert c.objective() == r.objective()
+    assert c.adjoint_steps(12) == r.adjoint_steps(12)
+    assert np.array_equal(c.v, r.get_state(1))
+    assert c.adjoint_steps(2, kernel=1) == r.adjoint_steps(2, kernel=1)
+    assert np.array_equal(c.v, r.get_state(1))
+    for kern in (0, 1):
+        gc, dc = c.gradient(kern)
+        gr, dr = r.gradient(kern)
+        assert np.array_equal(gc, gr) and dc == dr
+    assert c.penalty() == r.penalty()
+
+
+def test_restatement_one_shot_equals_reference(oracle_mod):
+    O = oracle_mod
+    _need_ref(O)
+    txt = case_text("exch2d")
+    ov = {"optimizer.zeta_stages": "0:0.002", "objective.penalty_w0": 0.001,
+          "objective.penalty_cap": 1.0, "objective.penalty_interval": 4,
+          "objective.penalty_growth": 2.0}
+    c, r = O.COracle(txt, ov), O.RefOracle(txt, ov)
+    c.init_state()
+    r.init_state()
+    rows = r.one_shot(9, 3)
+    lam = [min(0.001 * 2.0 ** ((it) / 4), 1.0) for it in range(1, 10)]
+    gms = [c.one_shot_iter(0.002, lam[i]) for i in range(9)]
+    assert np.array_equal(c.f, r.get_state(0))
+    assert np.array_equal(c.v, r.get_state(1))
+    t = r.tables()
+    assert np.array_equal(c.design(), t["w"])
+    assert rows[-1][6] == gms[-1]
+
+
+def test_golden_fixtures(oracle_mod):
+    """Known answers produced by the reference (make_golden.py) reproduce on
+    the restatement, so the oracle stays pinned where /root/reference is absent."""
+    O = oracle_mod
+    path = os.path.join(GOLDEN, "golden.npz")
+    g = np.load(path, allow_pickle=False)
+    for name in [str(s) for s in g["cases"]]:
+        c = O.COracle(case_text(name))
+        c.init_state()
+        c.primal_steps(int(g[f"{name}/primal_steps"]))
+        assert np.array_equal(c.f, g[f"{name}/f"]), name
+        c.adjoint_steps(int(g[f"{name}/adjoint_steps"]))
+        assert np.array_equal(c.v, g[f"{name}/v"]), name
+        gd, gdp = c.gradient()
+        assert np.array_equal(gd, g[f"{name}/grad"]) and gdp == float(g[f"{name}/grad_dp"])
+        assert c.objective() == float(g[f"{name}/objective"])
+
+
+def test_gradcheck_known_answer_restatement(oracle_mod):
+    """gradcheck2d converges to 1e-12 in 16,578 iterations with
+    objective 0.0126428346367474 (the reference, measured)."""
+    from paper_1501_04741_b200.presets import preset_text
+    c = oracle_mod.COracle(preset_text("gradcheck2d"))
+    c.init_state()
+    it = 0
+    while True:
+        it += 1
+        r = c.primal_steps(1)
+        if r <= 1e-12:
+            break
+    assert it == 16578
+    assert c.objective() == 0.012642834636747431
+
+
+def test_pairwise_sum_tree(oracle_mod):
+    """reduce.hpp:43-52: leaf 16, midpoint split — differs from a flat sum."""
+    x = np.random.default_rng(0).standard_normal(1000) * 1e8
+    s = oracle_mod.pairwise_sum(x)
+
+    def pw(lo, hi):
+        if hi - lo <= 16:
+            acc = 0.0
+            for i in range(lo, hi):
+                acc += float(x[i])
+            return acc
+        mid = lo + (hi - lo) // 2
+        return pw(lo, mid) + pw(mid, hi)
+    assert s == pw(0, 1000)
