@@ -67,7 +67,7 @@ _lib = None
 
 
 def build(verbose: bool = False) -> str:
-    from . import build as _b
+    from . import builder as _b
     return _b.build(verbose=verbose)
 
 
@@ -77,7 +77,7 @@ def load_library() -> C.CDLL:
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise LbgpuError(E_STATE, f"{LIB_PATH} is not built; run paper_1501_04741_b200/build.py")
+        raise LbgpuError(E_STATE, f"{LIB_PATH} is not built; run paper_1501_04741_b200/builder.py")
     L = C.CDLL(LIB_PATH)
     vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
     L.lbgpu_version.restype = C.c_char_p
