@@ -29,6 +29,7 @@
 #endif
 
 namespace lbgpu {
+namespace LBGPU_NS {  // per-build namespace: distinct kernel symbols per build
 
 namespace detail {
 
@@ -687,7 +688,6 @@ __global__ void k_init(long long N, R* __restrict__ buf) {
 
 // ---------------------------------------------------------------------
 // Host-side launchers (one set per build), dispatched by the engine.
-namespace LBGPU_NS {
 
 
 template <class L, class R, int CK, bool RES>
