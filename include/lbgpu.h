@@ -153,6 +153,12 @@ int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta,
 /* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of
  * `steps` back-to-back sweeps (no residual), bracketed by synchronisation. */
 int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms);
+/* `steps` x (one primal sweep then one adjoint sweep against it), one CUDA
+ * event between consecutive sweeps: total, primal-only and adjoint-only ms. */
+int lbgpu_time_pairs(lbgpu_engine* e, int64_t steps, double* ms_total, double* ms_primal,
+                     double* ms_adjoint);
+/* Number of sweep kernels this engine has launched. */
+int64_t lbgpu_sweep_launches(const lbgpu_engine* e);
 
 #ifdef __cplusplus
 }

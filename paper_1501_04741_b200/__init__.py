@@ -110,6 +110,9 @@ def load_library() -> C.CDLL:
     L.lbgpu_penalty.argtypes = [vp, dp]
     L.lbgpu_one_shot.argtypes = [vp, i64, vp, vp, i64, vp, i64, C.POINTER(i64)]
     L.lbgpu_time_sweeps.argtypes = [vp, C.c_int, i64, dp]
+    L.lbgpu_time_pairs.argtypes = [vp, i64, dp, dp, dp]
+    L.lbgpu_sweep_launches.argtypes = [vp]
+    L.lbgpu_sweep_launches.restype = i64
     _lib = L
     return L
 
@@ -303,6 +306,17 @@ class Engine:
         ms = C.c_double()
         self._ok(self.L.lbgpu_time_sweeps(self.h, which, steps, C.byref(ms)))
         return ms.value
+
+
+    def time_pairs(self, steps: int) -> tuple[float, float, float]:
+        """(total, primal, adjoint) milliseconds of `steps` primal+adjoint
+        sweep pairs, CUDA events between sweeps on the engine stream."""
+        t, p, a = C.c_double(), C.c_double(), C.c_double()
+        self._ok(self.L.lbgpu_time_pairs(self.h, steps, C.byref(t), C.byref(p), C.byref(a)))
+        return t.value, p.value, a.value
+
+    def sweep_launches(self) -> int:
+        return int(self.L.lbgpu_sweep_launches(self.h))
 
 
 def version() -> str:

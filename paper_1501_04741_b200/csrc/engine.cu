@@ -192,7 +192,7 @@ struct lbgpu_engine {
   std::vector<uint8_t> tag, mask, code;
   std::vector<double> w, bc_T, A, relax;
   std::vector<int8_t> bc_axis, bc_sign;
-  std::vector<long long> design, support, inlets;
+  std::vector<long long> design, support, inlets, faces;
   // device
   void* f[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -201,7 +201,7 @@ struct lbgpu_engine {
   uint8_t* d_code = nullptr;
   double *d_w = nullptr, *d_bcT = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
   double *d_A = nullptr, *d_At = nullptr;
-  long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr;
+  long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr, *d_faces = nullptr;
   double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
   double* d_ref = nullptr;
   unsigned long long* d_flags = nullptr;  // [resid, bad, aux]
@@ -211,6 +211,8 @@ struct lbgpu_engine {
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long primal_steps = 0, adjoint_steps = 0;
+  long long launches = 0;  // kernels this engine launched (sweeps + reductions + layout)
+  std::vector<cudaEvent_t> evs;  // per-sweep timing events (lbgpu_time_pairs)
   std::string err;
 
   size_t bytes_per_real() const { return prec == 64 ? 8 : 4; }
@@ -222,10 +224,12 @@ struct lbgpu_engine {
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
+    cudaFree(d_faces);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
     tree_support.release(), tree_design.release(), tree_inlet.release();
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (st) cudaStreamDestroy(st);
@@ -271,6 +275,7 @@ struct lbgpu_engine {
       if (!std::isfinite(bc_T[i])) throw Fail{LBGPU_E_CONFIG, "prescribed temperature is not finite"};
       if (mask[i]) design.push_back(i);
       if (tag[i] == TAG_INLET) inlets.push_back(i);
+      if (tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) faces.push_back(i);
     }
     M.obj_kind = d.obj_kind, M.flux_axis = d.flux_axis, M.flux_sign = d.flux_sign;
     if (d.obj_kind < 0 || d.obj_kind > 2) throw Fail{LBGPU_E_CONFIG, "unknown objective kind"};
@@ -315,6 +320,7 @@ struct lbgpu_engine {
     up_list(design, d_design);
     up_list(support, d_support);
     up_list(inlets, d_inlets);
+    up_list(faces, d_faces);
     const size_t nt = std::max({design.size(), support.size(), inlets.size(), size_t(1)});
     CU(cudaMalloc(&d_terms, sizeof(double) * nt));
     CU(cudaMalloc(&d_grad, sizeof(double) * std::max<size_t>(design.size(), 1)));
@@ -478,6 +484,7 @@ struct lbgpu_engine {
     s.a = launch(step);
     if (resid_slot) s.a.fl.resid = resid_slot;
     s.dim = dim, s.prec = prec, s.ck = ck, s.resid = resid;
+    s.faces = d_faces, s.n_faces = (long long)faces.size();
     return s;
   }
   void sync() { CU(cudaStreamSynchronize(st)); }
@@ -508,6 +515,7 @@ struct lbgpu_engine {
   // ------------------------------------------------------------ sweeps
   void primal_launch(bool resid, unsigned long long* slot) {
     ++primal_steps;
+    ++launches;
     const SweepArgs s = sweep(primal_steps, resid, slot);
     if (exact) exact::primal(s, f[fc], f[1 - fc]);
     else fast::primal(s, f[fc], f[1 - fc]);
@@ -515,6 +523,7 @@ struct lbgpu_engine {
   }
   void adjoint_launch(int kernel, bool resid, unsigned long long* slot) {
     ++adjoint_steps;
+    ++launches;
     const SweepArgs s = sweep(adjoint_steps, resid, slot);
     if (kernel) {
       if (exact) exact::adjoint_dual(s, f[fc], v[vc], v[1 - vc]);
@@ -877,6 +886,8 @@ int lbgpu_counters(const lbgpu_engine* e, int64_t* p, int64_t* a) {
   return LBGPU_OK;
 }
 
+int64_t lbgpu_sweep_launches(const lbgpu_engine* e) { return e ? e->launches : -1; }
+
 void* lbgpu_stream(const lbgpu_engine* e) { return e ? (void*)e->st : nullptr; }
 
 int lbgpu_init_state(lbgpu_engine* e) {
@@ -1024,6 +1035,44 @@ int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
     CU(cudaEventElapsedTime(&t, e->ev0, e->ev1));
     *ms = t;
     e->check_bad(which == 0 ? "iteration" : "adjoint iteration");
+  });
+}
+
+int lbgpu_time_pairs(lbgpu_engine* e, int64_t steps, double* ms_total, double* ms_primal,
+                     double* ms_adjoint) {
+  if (!ms_total || !ms_primal || !ms_adjoint || steps < 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    const size_t need = size_t(2 * steps + 1);
+    while (e->evs.size() < need) {
+      cudaEvent_t ev;
+      CU(cudaEventCreate(&ev));
+      e->evs.push_back(ev);
+    }
+    e->reset_flags();
+    e->sync();
+    CU(cudaEventRecord(e->evs[0], e->st));
+    for (int64_t k = 0; k < steps; ++k) {
+      e->primal_launch(false, nullptr);
+      CU(cudaEventRecord(e->evs[2 * k + 1], e->st));
+      e->adjoint_launch(0, false, nullptr);
+      CU(cudaEventRecord(e->evs[2 * k + 2], e->st));
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventSynchronize(e->evs[2 * steps]));
+    double tp = 0.0, ta = 0.0;
+    for (int64_t k = 0; k < steps; ++k) {
+      float a = 0.f, b = 0.f;
+      CU(cudaEventElapsedTime(&a, e->evs[2 * k], e->evs[2 * k + 1]));
+      CU(cudaEventElapsedTime(&b, e->evs[2 * k + 1], e->evs[2 * k + 2]));
+      tp += a;
+      ta += b;
+    }
+    float tot = 0.f;
+    CU(cudaEventElapsedTime(&tot, e->evs[0], e->evs[2 * steps]));
+    *ms_total = tot;
+    *ms_primal = tp;
+    *ms_adjoint = ta;
+    e->check_bad("iteration");
   });
 }
 

@@ -193,19 +193,28 @@ __device__ __forceinline__ double node_omt(const Model& M, const NodeTables& t, 
 // adjoint.cpp:50-121) in moment form: every contraction with d feq/d(rho,u)
 // is accumulated directly from w_j x_j, e_j . u and e_j . G u, and A^T = A
 // (symmetric for an orthogonal moment basis) is applied like the primal.
-template <class L, class R, int CK>
-__device__ __forceinline__ bool fast_vjp(const Model& M, PowPair pp, double omt, const R* f,
-                                         const R* g, const R* vf, const R* vg, R* outf, R* outg) {
-  R rho = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
+// Flow moments rho, j (and 1/rho) of one node's flow populations.
+template <class L, class R>
+__device__ __forceinline__ void flow_sums(const R* f, R& rho, R* j) {
+  R r = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
   LBGPU_FOR(J, 0, L::MF, {
-    rho += f[J];
+    r += f[J];
     if constexpr (L::ef(J, 0) != 0) j0 = L::ef(J, 0) > 0 ? j0 + f[J] : j0 - f[J];
     if constexpr (L::ef(J, 1) != 0) j1 = L::ef(J, 1) > 0 ? j1 + f[J] : j1 - f[J];
     if constexpr (L::ef(J, 2) != 0) j2 = L::ef(J, 2) > 0 ? j2 + f[J] : j2 - f[J];
   });
+  rho = r, j[0] = j0, j[1] = j1, j[2] = j2;
+}
+
+// The interior VJP reads the base state only through rho, u and T
+// (adjoint.cpp:59, :95): the moment-form entry point takes those.
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double omt, R rho,
+                                           const R* jv, R T, const R* vf, const R* vg, R* outf,
+                                           R* outg) {
   if (!(rho > R(0))) return false;
   const R inv = R(1) / rho;
-  const R u[3] = {j0 * inv, j1 * inv, j2 * inv};
+  const R u[3] = {jv[0] * inv, jv[1] * inv, jv[2] * inv};
   const R G = M.fluid_power ? R(pp.p0) : R(1.0 - pp.p0);
   const R up[3] = {G * u[0], G * u[1], G * u[2]};
   const R a0 = R(1) - R(1.5) * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
@@ -258,9 +267,8 @@ __device__ __forceinline__ bool fast_vjp(const Model& M, PowPair pp, double omt,
     Ru[a] = rho * (Ru[a] - R(3) * u[a] * R0);
   }
 
-  R T = R(0), St0 = R(0), St1[3] = {R(0), R(0), R(0)};
+  R St0 = R(0), St1[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MT, {
-    T += g[J];
     const R tw = R(L::wt(J)) * vg[J];
     St0 += tw;
     if constexpr (L::et(J, 0) != 0) St1[0] += L::et(J, 0) > 0 ? tw : -tw;
@@ -279,6 +287,37 @@ __device__ __forceinline__ bool fast_vjp(const Model& M, PowPair pp, double omt,
   const R om1 = R(1) - om, oms = om * sigma;
 #pragma unroll
   for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k] + oms;
+  return true;
+}
+
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_vjp(const Model& M, PowPair pp, double omt, const R* f,
+                                         const R* g, const R* vf, const R* vg, R* outf, R* outg) {
+  R rho, jv[3];
+  flow_sums<L, R>(f, rho, jv);
+  R T = R(0);
+#pragma unroll
+  for (int k = 0; k < L::MT; ++k) T += g[k];
+  return fast_vjp_m<L, R, CK>(M, pp, omt, rho, jv, T, vf, vg, outf, outg);
+}
+
+// node_partial (objective.cpp:34-62) from the node's moments.
+template <class L, class R>
+__device__ __forceinline__ bool fast_partial_m(const Model& M, R rho, const R* jv, R T, R* out) {
+  if (!(rho > R(0))) return false;
+  const R inv = R(1) / rho;
+  const int a = M.flux_axis;
+  const R ua = (a == 0 ? jv[0] : (a == 1 ? jv[1] : jv[2])) * inv;
+  const R sgn = R(M.flux_sign);
+  const R un = sgn * ua;
+  const R du = (M.obj_kind == 0 ? (R(1) - T * T) * sgn : T * sgn) * inv;
+  LBGPU_FOR(K_, 0, L::MF, {
+    const int ea = a == 0 ? L::ef(K_, 0) : (a == 1 ? L::ef(K_, 1) : L::ef(K_, 2));
+    out[K_] += du * (R(ea) - ua);
+  });
+  const R dT = M.obj_kind == 0 ? R(-2) * T * un : un;
+#pragma unroll
+  for (int k = 0; k < L::MT; ++k) out[L::MF + k] += dT;
   return true;
 }
 
@@ -404,10 +443,121 @@ __device__ __forceinline__ bool fast_face_vjp(const Model& M, PowPair pp, double
 // ====================================================================
 // Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
 
+namespace detail {
+
+__device__ __forceinline__ void idx_xyz(const Geom& g, long long idx, int& x, int& y, int& z) {
+  x = int(idx % g.nx);
+  y = int((idx / g.nx) % g.ny);
+  z = int(idx / ((long long)g.nx * g.ny));
+}
+
+__device__ __forceinline__ bool is_face(int tag) { return tag == TAG_INLET || tag == TAG_OUTLET; }
+
+// Store one node's M outputs and fold |new - old| into the thread's max.
+template <class L, class R, bool RESID>
+__device__ __forceinline__ void store_node(const R* __restrict__ src, R* __restrict__ dst,
+                                           long long N, long long idx, const R* in,
+                                           const R* out, unsigned long long& rmax) {
+  LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = out[P]; });
+  if constexpr (RESID) {
+    LBGPU_FOR(P, 0, L::M, {
+      constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
+      const R old = rest ? in[P] : __ldg(src + P * N + idx);
+      const unsigned long long d = absdiff_bits(double(out[P]), double(old));
+      rmax = d > rmax ? d : rmax;
+    });
+  }
+}
+
+// collide_node (collision.cpp:219-294) for one gathered node.
+template <class L, class R, int CK, bool FACES>
+__device__ __forceinline__ bool primal_node(const Launch& a, long long idx, uint8_t code,
+                                            const R* f, R* out) {
+  const int tag = code & TAG_MASK;
+  if (tag == TAG_WALL) {
+    LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
+    return true;
+  }
+  if (tag == TAG_HEATER) {
+    LBGPU_FOR(P, 0, L::MF, { out[P] = f[L::oppf(P)]; });
+    const R T = R(a.t.bcT[idx]);
+#pragma unroll
+    for (int j = 0; j < L::MT; ++j) out[L::MF + j] = R(L::wt(j)) * T * (R(1) + R(3) * R(0));
+    return true;
+  }
+  const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+  const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+#if LBGPU_EXACT
+  return collide_node<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f,
+                            R(w), R(a.M.rho_in), out);
+#else
+  const double omt = node_omt<R>(a.M, a.t, code, w);
+  if (!FACES || tag == TAG_INTERIOR) return fast_collide<L, R, CK>(a.M, pp, omt, f, out);
+  R rec[L::M];
+  face_recon<L, R>(a.M, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f, R(a.M.rho_in),
+                   rec, rec + L::MF);
+  return fast_collide<L, R, CK>(a.M, pp, omt, rec, out);
+#endif
+}
+
+// adjoint_collide_node (adjoint.cpp:156-204) for one node whose full base
+// state is at hand (bit-exact build, dual kernel, pressure faces).
+template <class L, class R, int CK, int AK>
+__device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx, uint8_t code,
+                                                  const R* fin, const R* vin, R* vout) {
+  const int tag = code & TAG_MASK;
+  bool ok = true;
+  if (AK == 0 && tag == TAG_WALL) {
+    LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+  } else if (AK == 0 && tag == TAG_HEATER) {
+    LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+#pragma unroll
+    for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
+  } else {
+    const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+    const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+    if (AK == 1 || (LBGPU_EXACT && tag != TAG_INTERIOR)) {
+      ok = vjp_dual<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], fin, R(w),
+                          vin, vout);
+    } else {
+#if LBGPU_EXACT
+      ok = interior_vjp<L, R>(a.M, pp, fin, fin + L::MF, R(w), vin, vin + L::MF, vout,
+                              vout + L::MF);
+#else
+      const double omt = node_omt<R>(a.M, a.t, code, w);
+      if (tag == TAG_INTERIOR)
+        ok = fast_vjp<L, R, CK>(a.M, pp, omt, fin, fin + L::MF, vin, vin + L::MF, vout,
+                                vout + L::MF);
+      else
+        ok = fast_face_vjp<L, R, CK>(a.M, pp, omt, tag, code_axis(code), code_sign(code),
+                                     a.t.bcT[idx], fin, vin, vout);
+#endif
+    }
+  }
+  if (code & CODE_SUPPORT) {
+    R b[L::M];
+    if (node_partial<L, R>(a.M, fin, b)) {
+#pragma unroll
+      for (int p = 0; p < L::M; ++p) vout[p] += b[p];
+    } else {
+      ok = false;
+    }
+  }
+  return ok;
+}
+
+}  // namespace detail
+
+// ====================================================================
+// Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
+// SPLIT: pressure-face nodes are left to the *_face kernels (one thread per
+// face node from a list), which keeps their heavy reconstruction out of the
+// bulk kernels' register allocation.
+
 // Primal sweep (primal_step, collision.cpp:308-363, in pull form) with the
 // node dispatch of collide_node (collision.cpp:219-294), the rho <= 0 flag
 // (collision.hpp:103) and, when RESID, the fused step_residual.
-template <class L, class R, int CK, bool RESID>
+template <class L, class R, int CK, bool RESID, bool SPLIT>
 __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
                                                 R* __restrict__ dst) {
   using namespace detail;
@@ -416,50 +566,39 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
   const int y = blockIdx.y, z = blockIdx.z;
   unsigned long long rmax = 0;
   if (x < g.x1) {
-    const long long N = g.N;
     const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
-    const Nbr nb = make_nbr(g, x, y, z);
-    R f[L::M];
-    gather<L, R, -1>(src, N, nb, f);
     const uint8_t code = a.t.code[idx];
-    const int tag = code & TAG_MASK;
-    R out[L::M];
-    bool ok = true;
-    if (tag == TAG_WALL) {
-      LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
-    } else if (tag == TAG_HEATER) {
-      LBGPU_FOR(P, 0, L::MF, { out[P] = f[L::oppf(P)]; });
-      const R T = R(a.t.bcT[idx]);
-#pragma unroll
-      for (int j = 0; j < L::MT; ++j) out[L::MF + j] = R(L::wt(j)) * T * (R(1) + R(3) * R(0));
-    } else {
-      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
-#if LBGPU_EXACT
-      ok = collide_node<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f,
-                              R(w), R(a.M.rho_in), out);
-#else
-      const double omt = node_omt<R>(a.M, a.t, code, w);
-      if (tag == TAG_INTERIOR) {
-        ok = fast_collide<L, R, CK>(a.M, pp, omt, f, out);
-      } else {
-        R rec[L::M];
-        face_recon<L, R>(a.M, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f,
-                         R(a.M.rho_in), rec, rec + L::MF);
-        ok = fast_collide<L, R, CK>(a.M, pp, omt, rec, out);
-      }
-#endif
+    if (!(SPLIT && is_face(code & TAG_MASK))) {
+      const Nbr nb = make_nbr(g, x, y, z);
+      R f[L::M], out[L::M];
+      gather<L, R, -1>(src, g.N, nb, f);
+      if (!primal_node<L, R, CK, !SPLIT>(a, idx, code, f, out))
+        atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+      store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax);
     }
-    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = out[P]; });
-    if constexpr (RESID) {
-      LBGPU_FOR(P, 0, L::M, {
-        constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
-        const R old = rest ? f[P] : __ldg(src + P * N + idx);
-        const unsigned long long d = absdiff_bits(double(out[P]), double(old));
-        rmax = d > rmax ? d : rmax;
-      });
-    }
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+}
+
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_primal_face(Launch a, const R* __restrict__ src,
+                                                     R* __restrict__ dst,
+                                                     const long long* __restrict__ faces,
+                                                     long long nf) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (i < nf) {
+    const long long idx = faces[i];
+    int x, y, z;
+    idx_xyz(g, idx, x, y, z);
+    const Nbr nb = make_nbr(g, x, y, z);
+    R f[L::M], out[L::M];
+    gather<L, R, -1>(src, g.N, nb, f);
+    if (!primal_node<L, R, CK, true>(a, idx, a.t.code[idx], f, out))
+      atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax);
   }
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
@@ -468,7 +607,9 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
 // against the links and the frozen base f along them, applies
 // adjoint_collide_node (adjoint.cpp:156-204) and stores the post-collision
 // adjoint. AK = 0 analytic kernel, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18).
-template <class L, class R, int CK, int AK, bool RESID>
+// Fast interior nodes reduce the gathered base to (rho, j, T) before the
+// adjoint populations are touched, so only ~M+5 values are live.
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
 __global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__ base,
                                                  const R* __restrict__ src,
                                                  R* __restrict__ dst) {
@@ -480,62 +621,74 @@ __global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__
   if (x < g.x1) {
     const long long N = g.N;
     const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
-    const Nbr nb = make_nbr(g, x, y, z);
-    R vin[L::M];
-    gather<L, R, +1>(src, N, nb, vin);
     const uint8_t code = a.t.code[idx];
     const int tag = code & TAG_MASK;
-    R vout[L::M];
-    bool ok = true;
-    R fin[L::M];
-    const bool need_base = AK == 1 || !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
-    if (need_base) gather<L, R, -1>(base, N, nb, fin);
-    if (AK == 0 && tag == TAG_WALL) {
-      LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
-    } else if (AK == 0 && tag == TAG_HEATER) {
-      LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
-#pragma unroll
-      for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
-    } else {
-      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
-      if (AK == 1 || (LBGPU_EXACT && tag != TAG_INTERIOR)) {
-        ok = vjp_dual<L, R>(a.M, pp, tag, code_axis(code), code_sign(code), a.t.bcT[idx], fin,
-                            R(w), vin, vout);
+    if (!(SPLIT && is_face(tag))) {
+      const Nbr nb = make_nbr(g, x, y, z);
+      R vin[L::M], vout[L::M];
+      bool ok = true;
+      // the synthetic objective's partial needs the populations themselves
+      if (LBGPU_EXACT || AK == 1 || is_face(tag) ||
+          ((code & CODE_SUPPORT) && a.M.obj_kind == 2)) {
+        R fin[L::M];
+        gather<L, R, -1>(base, N, nb, fin);
+        gather<L, R, +1>(src, N, nb, vin);
+        ok = adjoint_node_full<L, R, CK, AK>(a, idx, code, fin, vin, vout);
       } else {
-#if LBGPU_EXACT
-        ok = interior_vjp<L, R>(a.M, pp, fin, fin + L::MF, R(w), vin, vin + L::MF, vout,
-                                vout + L::MF);
-#else
-        const double omt = node_omt<R>(a.M, a.t, code, w);
-        if (tag == TAG_INTERIOR)
-          ok = fast_vjp<L, R, CK>(a.M, pp, omt, fin, fin + L::MF, vin, vin + L::MF, vout,
-                                  vout + L::MF);
-        else
-          ok = fast_face_vjp<L, R, CK>(a.M, pp, omt, tag, code_axis(code), code_sign(code),
-                                       a.t.bcT[idx], fin, vin, vout);
-#endif
-      }
-    }
-    if (code & CODE_SUPPORT) {
-      R b[L::M];
-      if (node_partial<L, R>(a.M, fin, b)) {
+        // moments of the base state (walls/heaters only need them on support nodes)
+        R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
+        const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
+        if (need) {
+          R fin[L::M];
+          gather<L, R, -1>(base, N, nb, fin);
+          flow_sums<L, R>(fin, rho, jv);
 #pragma unroll
-        for (int p = 0; p < L::M; ++p) vout[p] += b[p];
-      } else {
-        ok = false;
+          for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
+        }
+        gather<L, R, +1>(src, N, nb, vin);
+        if (tag == TAG_WALL) {
+          LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+        } else if (tag == TAG_HEATER) {
+          LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+#pragma unroll
+          for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
+        } else {
+          const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+          const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
+          const double omt = node_omt<R>(a.M, a.t, code, w);
+          ok = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout,
+                                    vout + L::MF);
+        }
+        if (code & CODE_SUPPORT) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
       }
+      if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+      store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
     }
-    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = vout[P]; });
-    if constexpr (RESID) {
-      LBGPU_FOR(P, 0, L::M, {
-        constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
-        const R old = rest ? vin[P] : __ldg(src + P * N + idx);
-        const unsigned long long d = absdiff_bits(double(vout[P]), double(old));
-        rmax = d > rmax ? d : rmax;
-      });
-    }
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+}
+
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_adjoint_face(Launch a, const R* __restrict__ base,
+                                                      const R* __restrict__ src,
+                                                      R* __restrict__ dst,
+                                                      const long long* __restrict__ faces,
+                                                      long long nf) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (i < nf) {
+    const long long idx = faces[i];
+    int x, y, z;
+    idx_xyz(g, idx, x, y, z);
+    const Nbr nb = make_nbr(g, x, y, z);
+    R fin[L::M], vin[L::M], vout[L::M];
+    gather<L, R, -1>(base, g.N, nb, fin);
+    gather<L, R, +1>(src, g.N, nb, vin);
+    if (!adjoint_node_full<L, R, CK, 0>(a, idx, a.t.code[idx], fin, vin, vout))
+      atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    store_node<L, R, RESID>(src, dst, g.N, idx, vin, vout, rmax);
   }
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
@@ -690,21 +843,34 @@ __global__ void k_init(long long N, R* __restrict__ buf) {
 // Host-side launchers (one set per build), dispatched by the engine.
 
 
+// Faces get their own kernel in the fast build (analytic adjoint kernel).
+constexpr bool kSplit = !LBGPU_EXACT;
+
 template <class L, class R, int CK, bool RES>
 void primal_t(const SweepArgs& s, const void* src, void* dst) {
   const Geom& g = s.a.g;
   const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
   dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
-  k_primal<L, R, CK, RES><<<grid, bx, 0, s.a.stream>>>(s.a, static_cast<const R*>(src),
-                                                        static_cast<R*>(dst));
+  const R* in = static_cast<const R*>(src);
+  R* out = static_cast<R*>(dst);
+  k_primal<L, R, CK, RES, kSplit><<<grid, bx, 0, s.a.stream>>>(s.a, in, out);
+  if (kSplit && s.n_faces > 0)
+    k_primal_face<L, R, CK, RES><<<unsigned((s.n_faces + 127) / 128), 128, 0, s.a.stream>>>(
+        s.a, in, out, s.faces, s.n_faces);
 }
 template <class L, class R, int CK, int AK, bool RES>
 void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst) {
   const Geom& g = s.a.g;
   const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
   dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
-  k_adjoint<L, R, CK, AK, RES><<<grid, bx, 0, s.a.stream>>>(
-      s.a, static_cast<const R*>(base), static_cast<const R*>(src), static_cast<R*>(dst));
+  const R* b = static_cast<const R*>(base);
+  const R* in = static_cast<const R*>(src);
+  R* out = static_cast<R*>(dst);
+  constexpr bool split = kSplit && AK == 0;
+  k_adjoint<L, R, CK, AK, RES, split><<<grid, bx, 0, s.a.stream>>>(s.a, b, in, out);
+  if (split && s.n_faces > 0)
+    k_adjoint_face<L, R, CK, RES><<<unsigned((s.n_faces + 127) / 128), 128, 0, s.a.stream>>>(
+        s.a, b, in, out, s.faces, s.n_faces);
 }
 
 #define LBGPU_CK_DISPATCH(...)                                        \
