@@ -192,7 +192,7 @@ struct lbgpu_engine {
   std::vector<uint8_t> tag, mask, code;
   std::vector<double> w, bc_T, A, relax;
   std::vector<int8_t> bc_axis, bc_sign;
-  std::vector<long long> design, support, inlets, faces;
+  std::vector<long long> design, support, inlets, adj_side;
   // device
   void* f[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -201,7 +201,8 @@ struct lbgpu_engine {
   uint8_t* d_code = nullptr;
   double *d_w = nullptr, *d_bcT = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
   double *d_A = nullptr, *d_At = nullptr;
-  long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr, *d_faces = nullptr;
+  long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr;
+  long long* d_adj_side = nullptr;
   double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
   double* d_ref = nullptr;
   unsigned long long* d_flags = nullptr;  // [resid, bad, aux]
@@ -224,7 +225,7 @@ struct lbgpu_engine {
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
-    cudaFree(d_faces);
+    cudaFree(d_adj_side);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -275,7 +276,6 @@ struct lbgpu_engine {
       if (!std::isfinite(bc_T[i])) throw Fail{LBGPU_E_CONFIG, "prescribed temperature is not finite"};
       if (mask[i]) design.push_back(i);
       if (tag[i] == TAG_INLET) inlets.push_back(i);
-      if (tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) faces.push_back(i);
     }
     M.obj_kind = d.obj_kind, M.flux_axis = d.flux_axis, M.flux_sign = d.flux_sign;
     if (d.obj_kind < 0 || d.obj_kind > 2) throw Fail{LBGPU_E_CONFIG, "unknown objective kind"};
@@ -320,7 +320,11 @@ struct lbgpu_engine {
     up_list(design, d_design);
     up_list(support, d_support);
     up_list(inlets, d_inlets);
-    up_list(faces, d_faces);
+    // adjoint side list: support nodes whose partial needs the full
+    // populations (synthetic objective) or that sit on a pressure face
+    for (long long i : support)
+      if (M.obj_kind == 2 || tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) adj_side.push_back(i);
+    up_list(adj_side, d_adj_side);
     const size_t nt = std::max({design.size(), support.size(), inlets.size(), size_t(1)});
     CU(cudaMalloc(&d_terms, sizeof(double) * nt));
     CU(cudaMalloc(&d_grad, sizeof(double) * std::max<size_t>(design.size(), 1)));
@@ -484,7 +488,7 @@ struct lbgpu_engine {
     s.a = launch(step);
     if (resid_slot) s.a.fl.resid = resid_slot;
     s.dim = dim, s.prec = prec, s.ck = ck, s.resid = resid;
-    s.faces = d_faces, s.n_faces = (long long)faces.size();
+    s.adj_side = d_adj_side, s.n_adj_side = (long long)adj_side.size();
     return s;
   }
   void sync() { CU(cudaStreamSynchronize(st)); }

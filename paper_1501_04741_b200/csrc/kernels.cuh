@@ -438,10 +438,165 @@ __device__ __forceinline__ bool fast_face_vjp(const Model& M, PowPair pp, double
   return true;
 }
 
-}  // namespace detail
 
-// ====================================================================
-// Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
+// ---------------------------------------------------------------------
+// In-place pressure-face treatment for the fast bulk kernels. The wet-node
+// collision of a Zou-He face is interior_collide applied to a reconstructed
+// input (collision.cpp:248-292); the face lane rebuilds its gathered
+// populations in place (compile-time normal axis AX and sign SG) and then
+// shares the interior collision / interior VJP with the other lanes of its
+// warp. The adjoint undoes the reconstruction by hand afterwards
+// (v <- J_recon^T v), again in place, from a handful of scalars.
+template <class R>
+struct FaceState {
+  R ua, rho, rho_t, Ksum, Tstar, tden;
+  bool clamped;
+};
+
+template <class L, class R, int AX, int SG>
+__device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet, double bcT,
+                                                     R* f) {
+  FaceState<R> fs;
+  R k0 = R(0), km = R(0);
+  LBGPU_FOR(J, 0, L::MF, {
+    constexpr int ea = L::ef(J, AX);
+    if constexpr (ea == 0) k0 += f[J];
+    if constexpr (ea == -SG) km += f[J];
+  });
+  const R s = R(SG);
+  fs.rho_t = R(inlet ? M.rho_in : M.rho_out);
+  fs.Ksum = k0 + R(2) * km;
+  R ua = s * (R(1) - fs.Ksum / fs.rho_t);
+  R rho = fs.rho_t;
+  fs.clamped = (ua < R(0) ? -ua : ua) > R(M.u_clamp);
+  if (fs.clamped) {
+    ua = ua > R(0) ? R(M.u_clamp) : R(-M.u_clamp);
+    rho = fs.Ksum / (R(1) - s * ua);
+  }
+  fs.ua = ua, fs.rho = rho;
+  // tangential momentum of the slots parallel to the face (collision.cpp:160-165)
+  R nb[3] = {R(0), R(0), R(0)};
+  LBGPU_FOR(J, 0, L::MF, {
+    if constexpr (L::ef(J, AX) == 0) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != AX && L::ef(J, b) != 0) nb[b] += R(0.5 * L::ef(J, b)) * f[J];
+    }
+  });
+  const R c0 = R(1) - R(1.5) * ua * ua;
+  LBGPU_FOR(J, 0, L::MF, {
+    if constexpr (L::ef(J, AX) == SG) {
+      constexpr int o = L::oppf(J);
+      const R eu = R(SG) * ua;
+      const R wr = R(L::wf(J)) * rho;
+      const R dfe = wr * (R(6) * eu);  // feq_j - feq_o: the even terms cancel
+      R corr = R(0);
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != AX && L::ef(J, b) != 0) corr += R(L::ef(J, b)) * nb[b];
+      f[J] = f[o] + dfe - corr;
+    }
+  });
+  (void)c0;
+  // thermal: imposed inlet temperature, or the outflow rebuild (collision.cpp:277-288)
+  R* g = f + L::MF;
+  if (inlet) {
+    fs.Tstar = R(bcT);
+    fs.tden = R(1);
+  } else {
+    R tnum = R(0), tden = R(0);
+    LBGPU_FOR(J, 0, L::MT, {
+      constexpr int ea = L::et(J, AX);
+      if constexpr (ea != SG) {
+        tnum += g[J];
+        tden += R(L::wt(J)) * (R(1) + R(3) * (R(ea) * ua));
+      }
+    });
+    fs.Tstar = tnum / tden;
+    fs.tden = tden;
+  }
+  LBGPU_FOR(J, 0, L::MT, {
+    constexpr int ea = L::et(J, AX);
+    g[J] = R(L::wt(J)) * fs.Tstar * (R(1) + R(3) * (R(ea) * ua));
+  });
+  return fs;
+}
+
+// v <- J_recon^T v for the reconstruction above (the branch the primal value
+// took at the u_clamp test, as the reference's dual sweep does).
+template <class L, class R, int AX, int SG>
+__device__ __forceinline__ void face_reverse(bool inlet, const FaceState<R>& fs, R* v) {
+  const R ua = fs.ua, rho = fs.rho, s = R(SG);
+  R arho = R(0), aua = R(0), anb[3] = {R(0), R(0), R(0)};
+  LBGPU_FOR(J, 0, L::MF, {
+    if constexpr (L::ef(J, AX) == SG) {
+      constexpr int o = L::oppf(J);
+      const R aj = v[J];
+      v[o] += aj;
+      v[J] = R(0);
+      // feq_j - feq_o = w rho 6 e ua  (e = SG): d/drho and d/dua
+      const R w = R(L::wf(J));
+      arho += aj * (w * R(6) * s * ua);
+      aua += aj * (w * rho * R(6) * s);
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != AX && L::ef(J, b) != 0) anb[b] -= aj * R(L::ef(J, b));
+    }
+  });
+  LBGPU_FOR(J, 0, L::MF, {
+    if constexpr (L::ef(J, AX) == 0) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != AX && L::ef(J, b) != 0) v[J] += R(0.5 * L::ef(J, b)) * anb[b];
+    }
+  });
+  R* vg = v + L::MF;
+  R aT = R(0);
+  LBGPU_FOR(J, 0, L::MT, {
+    constexpr int ea = L::et(J, AX);
+    const R tw = R(L::wt(J));
+    aT += vg[J] * tw * (R(1) + R(3) * (R(ea) * ua));
+    if constexpr (ea != 0) aua += vg[J] * tw * fs.Tstar * R(3 * ea);
+  });
+  if (inlet) {
+#pragma unroll
+    for (int j = 0; j < L::MT; ++j) vg[j] = R(0);
+  } else {
+    const R atnum = aT / fs.tden;
+    const R atden = -aT * fs.Tstar / fs.tden;
+    LBGPU_FOR(J, 0, L::MT, {
+      constexpr int ea = L::et(J, AX);
+      if constexpr (ea != SG) {
+        vg[J] = atnum;
+        if constexpr (ea != 0) aua += atden * R(L::wt(J)) * R(3 * ea);
+      } else {
+        vg[J] = R(0);
+      }
+    });
+  }
+  const R aK = fs.clamped ? arho / (R(1) - s * ua) : -aua * s / fs.rho_t;
+  LBGPU_FOR(J, 0, L::MF, {
+    constexpr int ea = L::ef(J, AX);
+    if constexpr (ea == 0) v[J] += aK;
+    if constexpr (ea == -SG) v[J] += R(2) * aK;
+  });
+}
+
+// Runtime (axis, sign) -> compile-time dispatch; 2D lattices have no z faces.
+template <class L, class F>
+__device__ __forceinline__ void face_dispatch(uint8_t code, F&& fn) {
+  const int ax = code_axis(code);
+  const bool neg = code & CODE_NEG;
+  if (ax == 0) {
+    if (neg) fn.template operator()<0, -1>(); else fn.template operator()<0, 1>();
+  } else if (ax == 1) {
+    if (neg) fn.template operator()<1, -1>(); else fn.template operator()<1, 1>();
+  } else if constexpr (L::DIM == 3) {
+    if (neg) fn.template operator()<2, -1>(); else fn.template operator()<2, 1>();
+  }
+}
+
+}  // namespace detail
 
 namespace detail {
 
@@ -457,12 +612,13 @@ __device__ __forceinline__ bool is_face(int tag) { return tag == TAG_INLET || ta
 template <class L, class R, bool RESID>
 __device__ __forceinline__ void store_node(const R* __restrict__ src, R* __restrict__ dst,
                                            long long N, long long idx, const R* in,
-                                           const R* out, unsigned long long& rmax) {
+                                           const R* out, unsigned long long& rmax,
+                                           bool in_valid = true) {
   LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = out[P]; });
   if constexpr (RESID) {
     LBGPU_FOR(P, 0, L::M, {
       constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
-      const R old = rest ? in[P] : __ldg(src + P * N + idx);
+      const R old = (rest && in_valid) ? in[P] : __ldg(src + P * N + idx);
       const unsigned long long d = absdiff_bits(double(out[P]), double(old));
       rmax = d > rmax ? d : rmax;
     });
@@ -472,7 +628,7 @@ __device__ __forceinline__ void store_node(const R* __restrict__ src, R* __restr
 // collide_node (collision.cpp:219-294) for one gathered node.
 template <class L, class R, int CK, bool FACES>
 __device__ __forceinline__ bool primal_node(const Launch& a, long long idx, uint8_t code,
-                                            const R* f, R* out) {
+                                            R* f, R* out) {
   const int tag = code & TAG_MASK;
   if (tag == TAG_WALL) {
     LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
@@ -492,11 +648,12 @@ __device__ __forceinline__ bool primal_node(const Launch& a, long long idx, uint
                             R(w), R(a.M.rho_in), out);
 #else
   const double omt = node_omt<R>(a.M, a.t, code, w);
-  if (!FACES || tag == TAG_INTERIOR) return fast_collide<L, R, CK>(a.M, pp, omt, f, out);
-  R rec[L::M];
-  face_recon<L, R>(a.M, tag, code_axis(code), code_sign(code), a.t.bcT[idx], f, R(a.M.rho_in),
-                   rec, rec + L::MF);
-  return fast_collide<L, R, CK>(a.M, pp, omt, rec, out);
+  if (FACES && is_face(tag)) {  // rebuild the face lane's inputs in place, then collide
+    const bool inlet = tag == TAG_INLET;
+    const double bcT = a.t.bcT[idx];
+    face_dispatch<L>(code, [&]<int AX, int SG>() { face_forward<L, R, AX, SG>(a.M, inlet, bcT, f); });
+  }
+  return fast_collide<L, R, CK>(a.M, pp, omt, f, out);
 #endif
 }
 
@@ -550,14 +707,13 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 
 // ====================================================================
 // Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
-// SPLIT: pressure-face nodes are left to the *_face kernels (one thread per
-// face node from a list), which keeps their heavy reconstruction out of the
-// bulk kernels' register allocation.
 
 // Primal sweep (primal_step, collision.cpp:308-363, in pull form) with the
 // node dispatch of collide_node (collision.cpp:219-294), the rho <= 0 flag
-// (collision.hpp:103) and, when RESID, the fused step_residual.
-template <class L, class R, int CK, bool RESID, bool SPLIT>
+// (collision.hpp:103) and, when RESID, the fused step_residual. Pressure-face
+// lanes rebuild their inputs in place (face_forward) and share the interior
+// collision with the rest of the warp.
+template <class L, class R, int CK, bool RESID>
 __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
                                                 R* __restrict__ dst) {
   using namespace detail;
@@ -568,37 +724,12 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
   if (x < g.x1) {
     const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
     const uint8_t code = a.t.code[idx];
-    if (!(SPLIT && is_face(code & TAG_MASK))) {
-      const Nbr nb = make_nbr(g, x, y, z);
-      R f[L::M], out[L::M];
-      gather<L, R, -1>(src, g.N, nb, f);
-      if (!primal_node<L, R, CK, !SPLIT>(a, idx, code, f, out))
-        atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-      store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax);
-    }
-  }
-  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
-}
-
-template <class L, class R, int CK, bool RESID>
-__global__ void __launch_bounds__(128) k_primal_face(Launch a, const R* __restrict__ src,
-                                                     R* __restrict__ dst,
-                                                     const long long* __restrict__ faces,
-                                                     long long nf) {
-  using namespace detail;
-  const Geom& g = a.g;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long rmax = 0;
-  if (i < nf) {
-    const long long idx = faces[i];
-    int x, y, z;
-    idx_xyz(g, idx, x, y, z);
     const Nbr nb = make_nbr(g, x, y, z);
     R f[L::M], out[L::M];
     gather<L, R, -1>(src, g.N, nb, f);
-    if (!primal_node<L, R, CK, true>(a, idx, a.t.code[idx], f, out))
+    if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
       atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax);
+    store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
   }
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
@@ -607,12 +738,16 @@ __global__ void __launch_bounds__(128) k_primal_face(Launch a, const R* __restri
 // against the links and the frozen base f along them, applies
 // adjoint_collide_node (adjoint.cpp:156-204) and stores the post-collision
 // adjoint. AK = 0 analytic kernel, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18).
-// Fast interior nodes reduce the gathered base to (rho, j, T) before the
-// adjoint populations are touched, so only ~M+5 values are live.
+// Fast build: the gathered base is reduced to (rho, j, T) before the adjoint
+// populations are loaded (the interior VJP reads f only through them,
+// adjoint.cpp:59, :95); face lanes rebuild / un-build in place. SPLIT leaves
+// the rare side-list nodes (synthetic-objective support, support nodes on a
+// face) to k_adjoint_side.
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__ base,
-                                                 const R* __restrict__ src,
-                                                 R* __restrict__ dst) {
+__global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint(Launch a,
+                                                                const R* __restrict__ base,
+                                                                const R* __restrict__ src,
+                                                                R* __restrict__ dst) {
   using namespace detail;
   const Geom& g = a.g;
   const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -623,24 +758,31 @@ __global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__
     const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
     const uint8_t code = a.t.code[idx];
     const int tag = code & TAG_MASK;
-    if (!(SPLIT && is_face(tag))) {
+    const bool face = is_face(tag);
+    const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
+    if (!(SPLIT && side)) {
       const Nbr nb = make_nbr(g, x, y, z);
       R vin[L::M], vout[L::M];
       bool ok = true;
-      // the synthetic objective's partial needs the populations themselves
-      if (LBGPU_EXACT || AK == 1 || is_face(tag) ||
-          ((code & CODE_SUPPORT) && a.M.obj_kind == 2)) {
+      if (LBGPU_EXACT || AK == 1 || !SPLIT) {
         R fin[L::M];
         gather<L, R, -1>(base, N, nb, fin);
         gather<L, R, +1>(src, N, nb, vin);
         ok = adjoint_node_full<L, R, CK, AK>(a, idx, code, fin, vin, vout);
       } else {
-        // moments of the base state (walls/heaters only need them on support nodes)
         R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
+        FaceState<R> fs{};
         const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
         if (need) {
           R fin[L::M];
           gather<L, R, -1>(base, N, nb, fin);
+          if (face) {
+            const bool inlet = tag == TAG_INLET;
+            const double bcT = a.t.bcT[idx];
+            face_dispatch<L>(code, [&]<int AX, int SG>() {
+              fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, fin);
+            });
+          }
           flow_sums<L, R>(fin, rho, jv);
 #pragma unroll
           for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
@@ -658,6 +800,12 @@ __global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__
           const double omt = node_omt<R>(a.M, a.t, code, w);
           ok = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout,
                                     vout + L::MF);
+          if (face) {
+            const bool inlet = tag == TAG_INLET;
+            face_dispatch<L>(code, [&]<int AX, int SG>() {
+              face_reverse<L, R, AX, SG>(inlet, fs, vout);
+            });
+          }
         }
         if (code & CODE_SUPPORT) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
       }
@@ -668,18 +816,19 @@ __global__ void __launch_bounds__(128) k_adjoint(Launch a, const R* __restrict__
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
+// Side-list adjoint nodes with the full (reference-form) node update.
 template <class L, class R, int CK, bool RESID>
-__global__ void __launch_bounds__(128) k_adjoint_face(Launch a, const R* __restrict__ base,
+__global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restrict__ base,
                                                       const R* __restrict__ src,
                                                       R* __restrict__ dst,
-                                                      const long long* __restrict__ faces,
-                                                      long long nf) {
+                                                      const long long* __restrict__ nodes,
+                                                      long long n) {
   using namespace detail;
   const Geom& g = a.g;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
-  if (i < nf) {
-    const long long idx = faces[i];
+  if (i < n) {
+    const long long idx = nodes[i];
     int x, y, z;
     idx_xyz(g, idx, x, y, z);
     const Nbr nb = make_nbr(g, x, y, z);
@@ -843,20 +992,13 @@ __global__ void k_init(long long N, R* __restrict__ buf) {
 // Host-side launchers (one set per build), dispatched by the engine.
 
 
-// Faces get their own kernel in the fast build (analytic adjoint kernel).
-constexpr bool kSplit = !LBGPU_EXACT;
-
 template <class L, class R, int CK, bool RES>
 void primal_t(const SweepArgs& s, const void* src, void* dst) {
   const Geom& g = s.a.g;
   const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
   dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
-  const R* in = static_cast<const R*>(src);
-  R* out = static_cast<R*>(dst);
-  k_primal<L, R, CK, RES, kSplit><<<grid, bx, 0, s.a.stream>>>(s.a, in, out);
-  if (kSplit && s.n_faces > 0)
-    k_primal_face<L, R, CK, RES><<<unsigned((s.n_faces + 127) / 128), 128, 0, s.a.stream>>>(
-        s.a, in, out, s.faces, s.n_faces);
+  k_primal<L, R, CK, RES><<<grid, bx, 0, s.a.stream>>>(s.a, static_cast<const R*>(src),
+                                                        static_cast<R*>(dst));
 }
 template <class L, class R, int CK, int AK, bool RES>
 void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst) {
@@ -866,11 +1008,11 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
   const R* b = static_cast<const R*>(base);
   const R* in = static_cast<const R*>(src);
   R* out = static_cast<R*>(dst);
-  constexpr bool split = kSplit && AK == 0;
+  constexpr bool split = !LBGPU_EXACT && AK == 0;
   k_adjoint<L, R, CK, AK, RES, split><<<grid, bx, 0, s.a.stream>>>(s.a, b, in, out);
-  if (split && s.n_faces > 0)
-    k_adjoint_face<L, R, CK, RES><<<unsigned((s.n_faces + 127) / 128), 128, 0, s.a.stream>>>(
-        s.a, b, in, out, s.faces, s.n_faces);
+  if (split && s.n_adj_side > 0)
+    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, s.a.stream>>>(
+        s.a, b, in, out, s.adj_side, s.n_adj_side);
 }
 
 #define LBGPU_CK_DISPATCH(...)                                        \

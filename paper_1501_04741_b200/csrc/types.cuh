@@ -43,8 +43,8 @@ struct SweepArgs {
   Launch a;
   int dim, prec, ck;  // ck: 0 bgk, 1 mrt (shear rows), 2 mrt + non-hydro rows
   bool resid;
-  const long long* faces;  // pressure-face nodes (local indices) for the face kernels
-  long long n_faces;
+  const long long* adj_side;  // adjoint side-list nodes (k_adjoint_side)
+  long long n_adj_side;
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).
