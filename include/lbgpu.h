@@ -68,6 +68,12 @@ typedef struct {
   int flux_axis, flux_sign;
   const int64_t* support; /* ascending flat indices */
   int64_t n_support;
+  /* x-slab decomposition (partition.cpp:9-21): with slab_count > 1 the engine
+   * owns global columns [x0, x0+span) of slab slab_id (decompose's sizes) and
+   * every per-node array above is in the local layout of lbgpu_slab_nxl(span)
+   * columns: owned at 0..span-1, right ghost at span, left ghost at nxl-1;
+   * support indices are local. nx stays the global extent. */
+  int slab_count, slab_id;
 } lbgpu_system_desc;
 
 /* One monitoring row (run_record.hpp:11-19): iteration, residual,
@@ -77,6 +83,9 @@ typedef struct {
 } lbgpu_run_row;
 
 const char* lbgpu_version(void);
+/* Local column count of a slab of `span` owned columns (span + 2 ghosts,
+ * rounded up to 16 so rows stay 128-byte aligned). */
+int lbgpu_slab_nxl(int span);
 
 /* --- lifecycle --- */
 int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out);
@@ -85,6 +94,9 @@ int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out);
  * and create the engine. exact as in lbgpu_system_desc. */
 int lbgpu_create_from_config(const char* cfg_text, const char* overrides, int device, int exact,
                              lbgpu_engine** out);
+/* One x-slab of the case: decompose(nx, slab_count)[slab_id] with local tables. */
+int lbgpu_create_slab_from_config(const char* cfg_text, const char* overrides, int device,
+                                  int exact, int slab_count, int slab_id, lbgpu_engine** out);
 void lbgpu_destroy(lbgpu_engine* e);
 /* Host-only: the System build_case would assemble from this case text, in
  * reference form (tags, bc arrays, design w/mask/nodes, support, A), without
@@ -92,6 +104,11 @@ void lbgpu_destroy(lbgpu_engine* e);
 int lbgpu_case_tables(const char* cfg_text, const char* overrides, int* dims, int64_t* counts,
                       uint8_t* tag, double* bc_T, int8_t* bc_axis, int8_t* bc_sign, double* w,
                       uint8_t* mask, int64_t* design, int64_t* support, double* A);
+/* Host-only slab variant (local layout). slab: gnx x0 span nxl count id. */
+int lbgpu_case_slab_tables(const char* cfg_text, const char* overrides, int slab_count,
+                           int slab_id, int* slab, int* dims, int64_t* counts, uint8_t* tag,
+                           double* bc_T, int8_t* bc_axis, int8_t* bc_sign, double* w,
+                           uint8_t* mask, int64_t* design, int64_t* support);
 const char* lbgpu_last_create_error(void);
 const char* lbgpu_error_message(const lbgpu_engine* e);
 
@@ -102,6 +119,8 @@ int lbgpu_info(const lbgpu_engine* e, int* dims, int64_t* counts);
 int lbgpu_get_tables(const lbgpu_engine* e, uint8_t* tag, double* bc_T, int8_t* bc_axis,
                      int8_t* bc_sign, double* w, uint8_t* mask, int64_t* design,
                      int64_t* support, double* A);
+/* gnx x0 span nxl slab_count slab_id */
+int lbgpu_slab_info(const lbgpu_engine* e, int* out6);
 /* Steps done since creation / the last reset. */
 int lbgpu_counters(const lbgpu_engine* e, int64_t* primal_steps, int64_t* adjoint_steps);
 /* The CUDA stream all work is issued on (cudaStream_t), for event timing. */
@@ -148,6 +167,25 @@ int lbgpu_penalty(lbgpu_engine* e, double* value);   /* penalty().value (topolog
 int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta,
                    const double* lambda, int64_t record_interval, lbgpu_run_row* rows,
                    int64_t cap, int64_t* n_rows);
+
+/* --- multi-slab runs (PartitionedRun, partition.cpp:43-312) --- */
+/* In-process group: engines[i] must be slab i of n (same device); they then
+ * share one stream and step in lock step through the lbgpu_group_* calls,
+ * each sweep followed by the halo exchange (neighbour buffers read directly). */
+int lbgpu_group_link(lbgpu_engine** engines, int n);
+/* which: 0 primal, 1 adjoint (kernel as lbgpu_adjoint_step); residual =
+ * global max-norm step residual of the last step (nullable). */
+int lbgpu_group_step(lbgpu_engine** engines, int n, int which, int64_t steps, int kernel,
+                     double* residual);
+/* Fill every slab's ghost columns of `field` (after uploads). */
+int lbgpu_group_exchange(lbgpu_engine** engines, int n, int field);
+/* NCCL (one slab per rank, one GPU per rank): rank 0 makes the id, every rank
+ * attaches with it; sweeps then exchange halos over NVLink and residuals /
+ * error flags are reduced across ranks. */
+int lbgpu_nccl_unique_id(void* out, int cap);
+int lbgpu_attach_nccl(lbgpu_engine* e, const void* unique_id, int nranks, int rank);
+/* Exchange the halos of `field` (collective in NCCL mode; after uploads). */
+int lbgpu_exchange(lbgpu_engine* e, int field);
 
 /* --- timing (device events on the engine stream; bench support) --- */
 /* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of

@@ -60,6 +60,7 @@ class SystemDesc(C.Structure):
         ("bc_sign", C.c_void_p), ("w", C.c_void_p), ("design_mask", C.c_void_p),
         ("obj_kind", C.c_int), ("flux_axis", C.c_int), ("flux_sign", C.c_int),
         ("support", C.c_void_p), ("n_support", C.c_int64),
+        ("slab_count", C.c_int), ("slab_id", C.c_int),
     ]
 
 
@@ -111,6 +112,16 @@ def load_library() -> C.CDLL:
     L.lbgpu_one_shot.argtypes = [vp, i64, vp, vp, i64, vp, i64, C.POINTER(i64)]
     L.lbgpu_time_sweeps.argtypes = [vp, C.c_int, i64, dp]
     L.lbgpu_time_pairs.argtypes = [vp, i64, dp, dp, dp]
+    L.lbgpu_slab_nxl.argtypes = [C.c_int]
+    L.lbgpu_create_slab_from_config.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                                C.c_int, C.POINTER(vp)]
+    L.lbgpu_slab_info.argtypes = [vp, C.POINTER(C.c_int)]
+    L.lbgpu_group_link.argtypes = [C.POINTER(vp), C.c_int]
+    L.lbgpu_group_step.argtypes = [C.POINTER(vp), C.c_int, C.c_int, i64, C.c_int, dp]
+    L.lbgpu_group_exchange.argtypes = [C.POINTER(vp), C.c_int, C.c_int]
+    L.lbgpu_nccl_unique_id.argtypes = [vp, C.c_int]
+    L.lbgpu_attach_nccl.argtypes = [vp, vp, C.c_int, C.c_int]
+    L.lbgpu_exchange.argtypes = [vp, C.c_int]
     L.lbgpu_sweep_launches.argtypes = [vp]
     L.lbgpu_sweep_launches.restype = i64
     _lib = L
@@ -186,6 +197,31 @@ class Engine:
         if rc:
             raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
         return cls(h.value)
+
+    @classmethod
+    def slab_from_config(cls, cfg_text: str, overrides: dict | None, slab_count: int,
+                         slab_id: int, device: int = 0, exact: bool = False) -> "Engine":
+        """Slab `slab_id` of decompose(nx, slab_count) (partition.cpp:9-21)."""
+        L = load_library()
+        ov = "\n".join(f"{k}={v}" for k, v in (overrides or {}).items()).encode()
+        h = C.c_void_p()
+        rc = L.lbgpu_create_slab_from_config(cfg_text.encode(), ov, device, int(exact),
+                                             slab_count, slab_id, C.byref(h))
+        if rc:
+            raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
+        return cls(h.value)
+
+    def slab(self) -> dict:
+        v = (C.c_int * 6)()
+        self._ok(self.L.lbgpu_slab_info(self.h, v))
+        return dict(zip(("gnx", "x0", "span", "nxl", "count", "id"), list(v)))
+
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        buf = C.create_string_buffer(unique_id, len(unique_id))
+        self._ok(self.L.lbgpu_attach_nccl(self.h, buf, nranks, rank))
+
+    def exchange(self, field: int) -> None:
+        self._ok(self.L.lbgpu_exchange(self.h, field))
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -317,6 +353,95 @@ class Engine:
 
     def sweep_launches(self) -> int:
         return int(self.L.lbgpu_sweep_launches(self.h))
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = C.create_string_buffer(256)
+    rc = L.lbgpu_nccl_unique_id(buf, 256)
+    if rc:
+        raise LbgpuError(rc, "ncclGetUniqueId failed")
+    return buf.raw[:128]
+
+
+class SlabGroup:
+    """In-process lock-step group of slab engines on one device (the
+    PartitionedRun of partition.cpp:43-312, with the halo exchange done by a
+    kernel that reads the neighbour slabs' buffers)."""
+
+    def __init__(self, cfg_text: str, overrides: dict | None, n: int, device: int = 0,
+                 exact: bool = False):
+        self.engines = [Engine.slab_from_config(cfg_text, overrides, n, i, device, exact)
+                        for i in range(n)]
+        self.L = load_library()
+        self._arr = (C.c_void_p * n)(*[e.h.value for e in self.engines])
+        rc = self.L.lbgpu_group_link(self._arr, n)
+        if rc:
+            raise LbgpuError(rc, "lbgpu_group_link failed")
+        self.n = n
+        self.slabs = [e.slab() for e in self.engines]
+        e0 = self.engines[0]
+        self.m, self.mf = e0.m, e0.mf
+        self.shape = (self.slabs[0]["gnx"], e0.shape[1], e0.shape[2])
+
+    def _ok(self, rc):
+        if rc:
+            raise LbgpuError(rc, self.L.lbgpu_error_message(self._arr[0]).decode())
+
+    def init_state(self):
+        for e in self.engines:
+            e.init_state()
+
+    def step(self, which: int, steps: int = 1, kernel: int = 0) -> float:
+        r = C.c_double()
+        self._ok(self.L.lbgpu_group_step(self._arr, self.n, which, steps, kernel, C.byref(r)))
+        return r.value
+
+    def exchange(self, field: int):
+        self._ok(self.L.lbgpu_group_exchange(self._arr, self.n, field))
+
+    def get_state(self, field: int) -> np.ndarray:
+        nx, ny, nz = self.shape
+        out = np.empty((self.m, nz, ny, nx))
+        for e, s in zip(self.engines, self.slabs):
+            loc = e.get_state(field).reshape(self.m, nz, ny, s["nxl"])
+            out[..., s["x0"]: s["x0"] + s["span"]] = loc[..., : s["span"]]
+        return out.reshape(-1)
+
+    def set_state(self, field: int, data: np.ndarray):
+        for e, s in zip(self.engines, self.slabs):
+            e.set_state(field, slab_cut(data, self.m, self.shape, s))
+        self.exchange(field)
+
+    def gradient(self, kernel: int = 0):
+        """Design gradient in global DesignField::nodes order + inlet_dp."""
+        idx, vals, gdp = [], [], 0.0
+        nx, ny, _ = self.shape
+        for e, s in zip(self.engines, self.slabs):
+            g, d = e.param_gradient(kernel)
+            loc = e.tables()["design"]
+            lx, rest = loc % s["nxl"], loc // s["nxl"]
+            idx.append(lx + s["x0"] + nx * rest)
+            vals.append(g)
+            gdp += d
+        idx = np.concatenate(idx)
+        order = np.argsort(idx, kind="stable")
+        return np.concatenate(vals)[order], gdp
+
+    def objective(self) -> float:
+        return sum(e.objective() for e in self.engines)
+
+
+def slab_cut(data: np.ndarray, m: int, shape, s: dict) -> np.ndarray:
+    """Local reference-layout array of slab s (owned columns + both ghosts)."""
+    nx, ny, nz = shape
+    g = np.asarray(data, np.float64).reshape(m, nz, ny, nx)
+    loc = np.zeros((m, nz, ny, s["nxl"]))
+    span, x0 = s["span"], s["x0"]
+    loc[..., :span] = g[..., x0: x0 + span]
+    loc[..., span] = g[..., (x0 + span) % nx]
+    loc[..., s["nxl"] - 1] = g[..., (x0 - 1) % nx]
+    return loc.reshape(-1)
 
 
 def version() -> str:

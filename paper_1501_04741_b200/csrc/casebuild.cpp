@@ -329,4 +329,98 @@ bool build_system(const CaseSpec& c, SystemArrays& s, std::string& err) {
   }
 }
 
+// One x-slab of the case (decompose, partition.cpp:9-21): the
+// tables of global columns [x0, x0+span) in a local array of nxl columns —
+// owned columns at local 0..span-1, the right ghost (global x0+span) at local
+// span, the left ghost (global x0-1) at local nxl-1, padding in between (so
+// rows stay aligned and the kernels' periodic wrap lands on the ghosts).
+// Values are those build_case gives the global lattice, including the
+// mt19937_64 design noise (drawn over all design nodes in global order).
+bool build_slab(const CaseSpec& c, int x0, int span, int nxl, SystemArrays& s, std::string& err) {
+  try {
+    if (span < 1 || x0 < 0 || x0 + span > c.nx || nxl < span + 2)
+      throw CfgError{"invalid slab geometry"};
+    const long n = long(nxl) * c.ny * c.nz;
+    const bool is3d = c.nz > 1;
+    s = SystemArrays{};
+    s.tag.assign(n, 1);
+    s.bc_T.assign(n, 0.0);
+    s.bc_axis.assign(n, 0);
+    s.bc_sign.assign(n, 0);
+    s.mask.assign(n, 0);
+    s.w.assign(n, 1.0);
+    const int hw = c.heater_x1 - c.heater_x0 + 1;
+    const int hz0 = is3d ? (c.nz - hw) / 2 : 0, hz1 = is3d ? hz0 + hw - 1 : 0;
+    auto gx_of = [&](int lx) {
+      if (lx < span) return x0 + lx;
+      if (lx == span) return (x0 + span) % c.nx;
+      if (lx == nxl - 1) return (x0 - 1 + c.nx) % c.nx;
+      return -1;
+    };
+    for (int z = 0; z < c.nz; ++z)
+      for (int y = 0; y < c.ny; ++y)
+        for (int lx = 0; lx < nxl; ++lx) {
+          const int x = gx_of(lx);
+          if (x < 0) continue;
+          const long i = lx + long(nxl) * (y + long(c.ny) * z);
+          uint8_t t = 0;
+          if (c.geometry != "periodic") {
+            if (y == 0 || y == c.ny - 1 || (is3d && (z == 0 || z == c.nz - 1))) {
+              t = 1;
+            } else if (x == 0) {
+              t = 2;
+              s.bc_sign[i] = 1;
+              s.bc_T[i] = c.inlet_profile == "split" ? (y < c.ny / 2 ? -1.0 : 1.0) : c.inlet_T;
+            } else if (x == c.nx - 1) {
+              t = 3;
+              s.bc_sign[i] = -1;
+            }
+            if (c.heater_x0 >= 0 && y == 0 && x >= c.heater_x0 && x <= c.heater_x1 && z >= hz0 &&
+                z <= hz1) {
+              t = 4;
+              s.bc_T[i] = 1.0;
+              s.bc_sign[i] = 0;
+            }
+          }
+          s.tag[i] = t;
+        }
+    // design: walk every global design node in ascending order, keep ours
+    std::mt19937_64 rng(c.seed);
+    if (c.design_x0 >= 0)
+      for (int z = 0; z < c.nz; ++z)
+        for (int y = 0; y < c.ny; ++y)
+          for (int x = c.design_x0; x <= c.design_x1; ++x) {
+            bool interior = true;
+            if (c.geometry != "periodic")
+              interior = !(y == 0 || y == c.ny - 1 || (is3d && (z == 0 || z == c.nz - 1)) ||
+                           x == 0 || x == c.nx - 1);
+            if (!interior) continue;
+            double w = c.initial_w;
+            if (c.init_noise > 0) {
+              const double u = double(rng() >> 11) * 0x1p-53;
+              w += c.init_noise * (2.0 * u - 1.0);
+            }
+            if (x >= x0 && x < x0 + span) {
+              const long i = (x - x0) + long(nxl) * (y + long(c.ny) * z);
+              s.mask[i] = 1;
+              s.w[i] = std::clamp(w, 0.0, 1.0);
+            }
+          }
+    s.obj_kind = c.objective == "mixing" ? 0 : (c.objective == "heatflux" ? 1 : 2);
+    s.flux_axis = 0;
+    s.flux_sign = 1;
+    const int xp = c.nx - 1 - c.plane_offset;
+    if (xp >= x0 && xp < x0 + span)
+      for (int z = 0; z < c.nz; ++z)
+        for (int y = 0; y < c.ny; ++y) {
+          const long i = (xp - x0) + long(nxl) * (y + long(c.ny) * z);
+          if (s.tag[i] == 0) s.support.push_back(i);
+        }
+    return true;
+  } catch (const CfgError& e) {
+    err = e.msg;
+    return false;
+  }
+}
+
 }  // namespace lbgpu

@@ -57,5 +57,16 @@ bool parse_case(const std::string& text, const std::string& overrides, CaseSpec&
                 std::string& err);
 // build_tags / build_design / build_objective.
 bool build_system(const CaseSpec& c, SystemArrays& out, std::string& err);
+// The same tables for one x-slab [x0, x0+span) in a local array of nxl
+// columns (owned at 0..span-1, right ghost at span, left ghost at nxl-1).
+bool build_slab(const CaseSpec& c, int x0, int span, int nxl, SystemArrays& out,
+                std::string& err);
+// decompose (partition.cpp:9-21): sizes differ by at most one, the first
+// nx % n slabs get the extra column.
+inline void decompose(int nx, int n, int id, int& x0, int& span) {
+  const int base = nx / n, rem = nx % n;
+  x0 = id * base + (id < rem ? id : rem);
+  span = base + (id < rem ? 1 : 0);
+}
 
 }  // namespace lbgpu

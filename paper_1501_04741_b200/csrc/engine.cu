@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/lbgpu.h"
 #include "casebuild.h"
 #include "types.cuh"
@@ -34,6 +37,50 @@ struct Fail {
       throw Fail{LBGPU_E_NUMERIC, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
                                       " (" #call ")"};                                   \
   } while (0)
+
+// NCCL is resolved at run time: a process that already loaded libnccl
+// (torch.distributed bundles its own) reuses that copy, so linking the
+// system library cannot shadow the one the host framework expects.
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const Nccl& nccl() {
+  static Nccl t = [] {
+    Nccl n{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) {
+      const char* env = getenv("LBGPU_NCCL_LIB");
+      h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) throw Fail{LBGPU_E_STATE, "libnccl.so.2 not found (set LBGPU_NCCL_LIB)"};
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p) throw Fail{LBGPU_E_STATE, std::string("NCCL symbol missing: ") + name};
+      return p;
+    };
+    n.GetUniqueId = (decltype(n.GetUniqueId))sym("ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))sym("ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))sym("ncclCommDestroy");
+    n.GroupStart = (decltype(n.GroupStart))sym("ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))sym("ncclGroupEnd");
+    n.Send = (decltype(n.Send))sym("ncclSend");
+    n.Recv = (decltype(n.Recv))sym("ncclRecv");
+    n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
+    n.GetErrorString = (decltype(n.GetErrorString))sym("ncclGetErrorString");
+    return n;
+  }();
+  return t;
+}
 
 constexpr unsigned long long kNoBad = ~0ull;
 constexpr unsigned long long kIdxMask = (1ull << 40) - 1;
@@ -183,6 +230,18 @@ using namespace lbgpu;
 struct lbgpu_engine {
   // shape / mode
   int nx = 0, ny = 0, nz = 0, dim = 2, mf = 0, mt = 0, m = 0, prec = 64, exact = 0, ck = 0;
+  // x-slab geometry: nx is the local array extent; owned
+  // columns are local 0..span-1 = global x0..x0+span-1.
+  int gnx = 0, x0 = 0, span = 0, slab_count = 1, slab_id = 0;
+  // halo exchange: 0 none (one slab, periodic wrap), 1 in-process group
+  // (neighbour buffers read directly), 2 NCCL (one slab per rank)
+  int xmode = 0;
+  lbgpu_engine* nb_left = nullptr;
+  lbgpu_engine* nb_right = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  void* halo_buf[4] = {nullptr, nullptr, nullptr, nullptr};  // send L, send R, recv L, recv R
+  bool owns_stream = true;
   long long N = 0;
   int device = 0;
   Model M{};
@@ -221,6 +280,8 @@ struct lbgpu_engine {
 
   ~lbgpu_engine() {
     if (!st) return;  // host-only instance (lbgpu_case_tables)
+    if (comm) nccl().CommDestroy(comm);
+    for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
@@ -233,7 +294,7 @@ struct lbgpu_engine {
     for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (st) cudaStreamDestroy(st);
+    if (st && owns_stream) cudaStreamDestroy(st);
   }
 
   // ------------------------------------------------------------ setup
@@ -243,10 +304,22 @@ struct lbgpu_engine {
     if (d.precision != 64 && d.precision != 32) throw Fail{LBGPU_E_CONFIG, "precision must be 32 or 64"};
     if (d.exact && d.precision != 64)
       throw Fail{LBGPU_E_CONFIG, "the bit-exact build is double precision only"};
-    if (!d.tag || !d.bc_T || !d.bc_axis || !d.bc_sign || !d.w || !d.design_mask || !d.support)
+    if (!d.tag || !d.bc_T || !d.bc_axis || !d.bc_sign || !d.w || !d.design_mask ||
+        (!d.support && d.n_support > 0))
       throw Fail{LBGPU_E_ARG, "system description is missing a per-node table"};
     nx = d.nx, ny = d.ny, nz = d.nz, prec = d.precision, exact = d.exact ? 1 : 0;
     device = d.device;
+    gnx = d.nx;
+    slab_count = d.slab_count > 1 ? d.slab_count : 1;
+    slab_id = slab_count > 1 ? d.slab_id : 0;
+    if (slab_count > 1) {
+      if (slab_id < 0 || slab_id >= slab_count) throw Fail{LBGPU_E_CONFIG, "slab id out of range"};
+      if (slab_count > gnx) throw Fail{LBGPU_E_CONFIG, "more workers than lattice columns"};
+      decompose(gnx, slab_count, slab_id, x0, span);
+      nx = lbgpu_slab_nxl(span);
+    } else {
+      x0 = 0, span = gnx;
+    }
     N = (long long)nx * ny * nz;
     dim = nz == 1 ? 2 : 3;
     mf = dim == 2 ? LatD2::MF : LatD3::MF;
@@ -274,12 +347,13 @@ struct lbgpu_engine {
           throw Fail{LBGPU_E_CONFIG, "pressure node normal sign must be +1 or -1"};
       }
       if (!std::isfinite(bc_T[i])) throw Fail{LBGPU_E_CONFIG, "prescribed temperature is not finite"};
-      if (mask[i]) design.push_back(i);
-      if (tag[i] == TAG_INLET) inlets.push_back(i);
+      const bool owned = (i % nx) < span;
+      if (mask[i] && owned) design.push_back(i);
+      if (tag[i] == TAG_INLET && owned) inlets.push_back(i);
     }
     M.obj_kind = d.obj_kind, M.flux_axis = d.flux_axis, M.flux_sign = d.flux_sign;
     if (d.obj_kind < 0 || d.obj_kind > 2) throw Fail{LBGPU_E_CONFIG, "unknown objective kind"};
-    support.assign(d.support, d.support + d.n_support);
+    if (d.n_support > 0) support.assign(d.support, d.support + d.n_support);
     for (size_t k = 0; k < support.size(); ++k)
       if (support[k] < 0 || support[k] >= N || (k && support[k] <= support[k - 1]))
         throw Fail{LBGPU_E_CONFIG, "objective support must be ascending node indices"};
@@ -342,7 +416,7 @@ struct lbgpu_engine {
       refresh_pow_tables();
     }
     T.code = d_code, T.w = d_w, T.bcT = d_bcT, T.p0 = d_p0, T.p1 = d_p1;
-    G = Geom{nx, ny, nz, 0, nx, N, 0, nx, ny};
+    G = Geom{nx, ny, nz, 0, span, N, x0, gnx, ny};
     init_state();
     CU(cudaStreamSynchronize(st));
   }
@@ -517,15 +591,16 @@ struct lbgpu_engine {
   }
 
   // ------------------------------------------------------------ sweeps
-  void primal_launch(bool resid, unsigned long long* slot) {
+  void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
     ++primal_steps;
     ++launches;
     const SweepArgs s = sweep(primal_steps, resid, slot);
     if (exact) exact::primal(s, f[fc], f[1 - fc]);
     else fast::primal(s, f[fc], f[1 - fc]);
     fc ^= 1;
+    if (exch && xmode == 2) exchange(0);
   }
-  void adjoint_launch(int kernel, bool resid, unsigned long long* slot) {
+  void adjoint_launch(int kernel, bool resid, unsigned long long* slot, bool exch = true) {
     ++adjoint_steps;
     ++launches;
     const SweepArgs s = sweep(adjoint_steps, resid, slot);
@@ -537,6 +612,57 @@ struct lbgpu_engine {
       else fast::adjoint(s, f[fc], v[vc], v[1 - vc]);
     }
     vc ^= 1;
+    if (exch && xmode == 2) exchange(1);
+  }
+
+  // ------------------------------------------------------------ halo
+  void* cur(int field) const { return field == 0 ? f[fc] : v[vc]; }
+  size_t halo_bytes() const { return bytes_per_real() * 6 * size_t(ny) * nz; }
+  void ensure_halo_bufs() {
+    for (void*& h : halo_buf)
+      if (!h) CU(cudaMalloc(&h, halo_bytes()));
+  }
+  void halo_op(int op, int field, void* a, void* b, const lbgpu_engine* l, const lbgpu_engine* r) {
+    const Geom gl = l ? l->G : G, gr = r ? r->G : G;
+    const void* lb = l ? l->cur(field) : nullptr;
+    const void* rb = r ? r->cur(field) : nullptr;
+    if (exact) exact::halo(op, G, dim, prec, field, cur(field), a, b, lb, gl, rb, gr, st);
+    else fast::halo(op, G, dim, prec, field, cur(field), a, b, lb, gl, rb, gr, st);
+    ++launches;
+  }
+  // Fill this slab's ghost columns of `field` after a sweep of it.
+  void exchange(int field) {
+    if (xmode == 1) {
+      halo_op(2, field, nullptr, nullptr, nb_left, nb_right);
+    } else if (xmode == 2) {
+      ensure_halo_bufs();
+      halo_op(0, field, halo_buf[0], halo_buf[1], nullptr, nullptr);
+      const size_t cnt = halo_bytes() / bytes_per_real();
+      const ncclDataType_t ty = prec == 64 ? ncclFloat64 : ncclFloat32;
+      const int left = (rank - 1 + nranks) % nranks, right = (rank + 1) % nranks;
+      // posting order per peer is the same on every rank, so with two ranks
+      // (left == right) the i-th send meets the i-th receive
+      const Nccl& N_ = nccl();
+      N_.GroupStart();
+      N_.Send(halo_buf[1], cnt, ty, right, comm, st);
+      N_.Recv(halo_buf[2], cnt, ty, left, comm, st);
+      N_.Send(halo_buf[0], cnt, ty, left, comm, st);
+      N_.Recv(halo_buf[3], cnt, ty, right, comm, st);
+      const ncclResult_t r = N_.GroupEnd();
+      if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + N_.GetErrorString(r)};
+      halo_op(1, field, halo_buf[2], halo_buf[3], nullptr, nullptr);
+    }
+  }
+  // Global max / min of device flag words across ranks (NCCL mode).
+  void reduce_flags(unsigned long long* d, size_t n, bool is_min) {
+    if (xmode != 2) return;
+    const ncclResult_t r =
+        nccl().AllReduce(d, d, n, ncclUint64, is_min ? ncclMin : ncclMax, comm, st);
+    if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + nccl().GetErrorString(r)};
+  }
+  void require_solo() const {
+    if (xmode == 1)
+      throw Fail{LBGPU_E_STATE, "slab engine in an in-process group: use lbgpu_group_* calls"};
   }
 
   void init_state() {
@@ -547,6 +673,7 @@ struct lbgpu_engine {
   }
 
   double steps(int which, long long n, int kernel, bool want_resid) {
+    require_solo();
     if (n <= 0) return 0.0;
     reset_flags();
     for (long long k = 0; k < n; ++k) {
@@ -555,6 +682,8 @@ struct lbgpu_engine {
       else adjoint_launch(kernel, r, nullptr);
     }
     CU(cudaGetLastError());
+    reduce_flags(d_flags, 1, false);
+    reduce_flags(d_flags + 1, 1, true);
     pull_flags();
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], which == 0 ? "iteration" : "adjoint iteration");
     return want_resid ? bits_to_double(h_flags[0]) : 0.0;
@@ -567,6 +696,7 @@ struct lbgpu_engine {
   // and final state are exactly the per-step loop's.
   void solve(int which, double tol, long long max_iter, long long fixed, int kernel,
              long long* iters, double* resid, int* conv) {
+    require_solo();
     const long long n = fixed >= 0 ? fixed : max_iter;
     const char* what = which == 0 ? "iteration" : "adjoint iteration";
     if (which == 1) {
@@ -591,6 +721,8 @@ struct lbgpu_engine {
         else adjoint_launch(kernel, true, d_ring + k);
       }
       CU(cudaGetLastError());
+      reduce_flags(d_ring, size_t(b), false);
+      reduce_flags(d_flags + 1, 1, true);
       CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
       CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long) * b, cudaMemcpyDeviceToHost, st));
       sync();
@@ -683,6 +815,7 @@ struct lbgpu_engine {
 
   void one_shot(long long iters, const double* zeta, const double* lambda, long long ri,
                 lbgpu_run_row* rows, long long cap, long long* nrows) {
+    require_solo();
     long long k = 0;
     reset_flags();
     const long long n = (long long)design.size();
@@ -702,6 +835,9 @@ struct lbgpu_engine {
         refresh_pow_tables();
       }
       if (rec) {
+        reduce_flags(d_flags, 1, false);
+        reduce_flags(d_flags + 2, 1, false);
+        reduce_flags(d_flags + 1, 1, true);
         pull_flags();
         if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
         lbgpu_run_row row;
@@ -768,6 +904,110 @@ extern "C" {
 
 const char* lbgpu_version(void) { return "0.1.0-b200"; }
 
+int lbgpu_slab_nxl(int span) { return (span + 2 + 15) / 16 * 16; }
+
+int lbgpu_slab_info(const lbgpu_engine* e, int* out6) {
+  if (!e || !out6) return LBGPU_E_ARG;
+  const int v[6] = {e->gnx, e->x0, e->span, e->nx, e->slab_count, e->slab_id};
+  std::memcpy(out6, v, sizeof v);
+  return LBGPU_OK;
+}
+
+int lbgpu_group_link(lbgpu_engine** es, int n) {
+  if (!es || n < 1) return LBGPU_E_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!es[i] || es[i]->slab_count != n || es[i]->slab_id != i || es[i]->device != es[0]->device)
+      return LBGPU_E_ARG;
+  if (n == 1) return LBGPU_OK;
+  for (int i = 0; i < n; ++i) {
+    lbgpu_engine* e = es[i];
+    if (i > 0) {  // share slab 0's stream: lock-step order is stream order
+      cudaSetDevice(e->device);
+      cudaStreamSynchronize(e->st);
+      if (e->owns_stream) cudaStreamDestroy(e->st);
+      e->st = es[0]->st;
+      e->owns_stream = false;
+    }
+    e->xmode = 1;
+    e->nb_left = es[(i - 1 + n) % n];
+    e->nb_right = es[(i + 1) % n];
+  }
+  return LBGPU_OK;
+}
+
+int lbgpu_group_exchange(lbgpu_engine** es, int n, int field) {
+  if (!es || n < 1 || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  for (int i = 0; i < n; ++i) {
+    const int rc = guarded(es[i], [&] { es[i]->exchange(field); });
+    if (rc) return rc;
+  }
+  return guarded(es[0], [&] { es[0]->sync(); });
+}
+
+int lbgpu_group_step(lbgpu_engine** es, int n, int which, int64_t steps, int kernel,
+                     double* residual) {
+  if (!es || n < 1 || steps < 0 || (which != 0 && which != 1)) return LBGPU_E_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!es[i] || (n > 1 && es[i]->xmode != 1)) return LBGPU_E_STATE;
+  return guarded(es[0], [&] {
+    for (int i = 0; i < n; ++i) es[i]->reset_flags();
+    for (int64_t k = 0; k < steps; ++k) {
+      const bool r = residual && k == steps - 1;
+      for (int i = 0; i < n; ++i) {
+        if (which == 0) es[i]->primal_launch(r, nullptr, false);
+        else es[i]->adjoint_launch(kernel, r, nullptr, false);
+      }
+      if (n > 1)
+        for (int i = 0; i < n; ++i) es[i]->exchange(which);
+    }
+    CU(cudaGetLastError());
+    double rmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      es[i]->pull_flags();
+      if (es[i]->h_flags[1] != kNoBad)
+        es[i]->raise_bad(es[i]->h_flags[1], which == 0 ? "iteration" : "adjoint iteration");
+      const double ri = lbgpu_engine::bits_to_double(es[i]->h_flags[0]);
+      if (!(ri <= rmax)) rmax = ri;
+    }
+    if (residual) *residual = rmax;
+  });
+}
+
+int lbgpu_nccl_unique_id(void* out, int cap) {
+  if (!out || cap < (int)sizeof(ncclUniqueId)) return LBGPU_E_ARG;
+  ncclUniqueId id;
+  try {
+    if (nccl().GetUniqueId(&id) != ncclSuccess) return LBGPU_E_NUMERIC;
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    return f.code;
+  }
+  std::memcpy(out, &id, sizeof id);
+  return LBGPU_OK;
+}
+
+int lbgpu_attach_nccl(lbgpu_engine* e, const void* uid, int nranks, int rank) {
+  if (!uid || nranks < 1 || rank < 0 || rank >= nranks) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    if (e->slab_count != nranks || e->slab_id != rank)
+      throw Fail{LBGPU_E_CONFIG, "engine must be slab `rank` of `nranks`"};
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    const ncclResult_t r = nccl().CommInitRank(&e->comm, nranks, id, rank);
+    if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + nccl().GetErrorString(r)};
+    e->rank = rank, e->nranks = nranks;
+    e->xmode = nranks > 1 ? 2 : 0;
+  });
+}
+
+int lbgpu_exchange(lbgpu_engine* e, int field) {
+  if (field != 0 && field != 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->exchange(field);
+    e->sync();
+  });
+}
+
 int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out) {
   if (!desc || !out) return LBGPU_E_ARG;
   *out = nullptr;
@@ -789,13 +1029,31 @@ int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out) {
 }
 
 static int desc_from_config(const char* cfg_text, const char* overrides, int device, int exact,
-                            CaseSpec& c, SystemArrays& s, lbgpu_system_desc& d) {
+                            CaseSpec& c, SystemArrays& s, lbgpu_system_desc& d,
+                            int slab_count = 1, int slab_id = 0) {
   std::string err;
-  if (!parse_case(cfg_text, overrides ? overrides : "", c, err) || !build_system(c, s, err)) {
+  if (!parse_case(cfg_text, overrides ? overrides : "", c, err)) {
+    g_create_err = err;
+    return LBGPU_E_CONFIG;
+  }
+  bool ok;
+  if (slab_count > 1) {
+    if (slab_id < 0 || slab_id >= slab_count || slab_count > c.nx) {
+      g_create_err = "invalid slab decomposition";
+      return LBGPU_E_CONFIG;
+    }
+    int x0, span;
+    decompose(c.nx, slab_count, slab_id, x0, span);
+    ok = build_slab(c, x0, span, lbgpu_slab_nxl(span), s, err);
+  } else {
+    ok = build_system(c, s, err);
+  }
+  if (!ok) {
     g_create_err = err;
     return LBGPU_E_CONFIG;
   }
   d = lbgpu_system_desc{};
+  d.slab_count = slab_count, d.slab_id = slab_id;
   d.nx = c.nx, d.ny = c.ny, d.nz = c.nz;
   d.precision = c.precision;
   d.exact = exact;
@@ -823,6 +1081,48 @@ int lbgpu_create_from_config(const char* cfg_text, const char* overrides, int de
   const int rc = desc_from_config(cfg_text, overrides, device, exact, c, s, d);
   if (rc) return rc;
   return lbgpu_create(&d, out);
+}
+
+int lbgpu_create_slab_from_config(const char* cfg_text, const char* overrides, int device,
+                                  int exact, int slab_count, int slab_id, lbgpu_engine** out) {
+  if (!cfg_text || !out) return LBGPU_E_ARG;
+  *out = nullptr;
+  g_create_err.clear();
+  CaseSpec c;
+  SystemArrays s;
+  lbgpu_system_desc d;
+  const int rc = desc_from_config(cfg_text, overrides, device, exact, c, s, d, slab_count, slab_id);
+  if (rc) return rc;
+  return lbgpu_create(&d, out);
+}
+
+int lbgpu_case_slab_tables(const char* cfg_text, const char* overrides, int slab_count,
+                           int slab_id, int* slab, int* dims, int64_t* counts, uint8_t* tag,
+                           double* bc_T, int8_t* bc_axis, int8_t* bc_sign, double* w,
+                           uint8_t* mask, int64_t* design, int64_t* support) {
+  if (!cfg_text || !slab || !dims || !counts) return LBGPU_E_ARG;
+  g_create_err.clear();
+  CaseSpec c;
+  SystemArrays s;
+  lbgpu_system_desc d;
+  const int rc = desc_from_config(cfg_text, overrides, 0, 0, c, s, d, slab_count, slab_id);
+  if (rc) return rc;
+  lbgpu_engine e;
+  try {
+    e.setup_host(d);
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    return f.code;
+  }
+  const int sl[6] = {e.gnx, e.x0, e.span, e.nx, e.slab_count, e.slab_id};
+  std::memcpy(slab, sl, sizeof sl);
+  const int dd[8] = {e.nx, e.ny, e.nz, e.m, e.mf, e.mt, e.prec, 0};
+  std::memcpy(dims, dd, sizeof dd);
+  counts[0] = e.N;
+  counts[1] = (int64_t)e.design.size();
+  counts[2] = (int64_t)e.support.size();
+  counts[3] = (int64_t)e.inlets.size();
+  return lbgpu_get_tables(&e, tag, bc_T, bc_axis, bc_sign, w, mask, design, support, nullptr);
 }
 
 int lbgpu_case_tables(const char* cfg_text, const char* overrides, int* dims, int64_t* counts,
@@ -914,6 +1214,7 @@ int lbgpu_upload_state(lbgpu_engine* e, int field, const double* ref) {
     e->ensure_ref();
     CU(cudaMemcpyAsync(e->d_ref, ref, sizeof(double) * e->m * e->N, cudaMemcpyHostToDevice, e->st));
     e->from_ref(field, e->d_ref);
+    if (e->xmode == 2) e->exchange(field);  // ghosts (collective: every rank uploads)
     e->sync();
   });
 }

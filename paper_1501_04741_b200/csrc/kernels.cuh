@@ -989,6 +989,77 @@ __global__ void k_init(long long N, R* __restrict__ buf) {
 }
 
 // ---------------------------------------------------------------------
+// Halo exchange between x-slabs (PartitionedRun::do_step's pack / send /
+// recv / install, partition.cpp:133-174, in pull form). After a sweep of a
+// field with pull direction D (-1 primal, +1 adjoint), the next sweep's
+// owned column 0 reads the planes with D*e_x = -1 from the left ghost
+// (local nx-1) and column span-1 reads the planes with D*e_x = +1 from the
+// right ghost (local span). So each slab ships its last owned column's
+// D*e_x = -1 planes to the right neighbour and its first column's
+// D*e_x = +1 planes to the left neighbour: 6 planes x ny x nz each way for
+// both lattice pairs. For the adjoint (D = +1) these are the primal's lists
+// swapped, the reference's transposed plan (partition.cpp:143-146).
+template <class L, int D, int S>
+__device__ __forceinline__ constexpr int halo_slot(int k) {
+  int c = 0;
+  for (int p = 0; p < L::M; ++p)
+    if (D * cvel<L>(p, 0) == S) {
+      if (c == k) return p;
+      ++c;
+    }
+  return -1;
+}
+template <class L>
+constexpr int kHaloPlanes = 6;  // D2Q9+D2Q9: 3+3, D3Q19+D3Q7: 5+1
+
+template <class L, class R, int D>
+__global__ void k_halo_pack(Geom g, const R* __restrict__ buf, R* __restrict__ send_left,
+                            R* __restrict__ send_right) {
+  const long long yz = (long long)g.ny * g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= yz) return;
+  const long long row = (long long)g.nx * t;  // node (0, y, z) with t = y + ny*z
+#pragma unroll
+  for (int k = 0; k < kHaloPlanes<L>; ++k) {
+    const int pr = halo_slot<L, D, -1>(k), pl = halo_slot<L, D, +1>(k);
+    send_right[k * yz + t] = buf[pr * g.N + row + (g.x1 - 1)];
+    send_left[k * yz + t] = buf[pl * g.N + row + g.x0];
+  }
+}
+
+template <class L, class R, int D>
+__global__ void k_halo_unpack(Geom g, R* __restrict__ buf, const R* __restrict__ recv_left,
+                              const R* __restrict__ recv_right) {
+  const long long yz = (long long)g.ny * g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= yz) return;
+  const long long row = (long long)g.nx * t;
+#pragma unroll
+  for (int k = 0; k < kHaloPlanes<L>; ++k) {
+    const int pr = halo_slot<L, D, -1>(k), pl = halo_slot<L, D, +1>(k);
+    buf[pr * g.N + row + (g.nx - 1)] = recv_left[k * yz + t];
+    buf[pl * g.N + row + g.x1] = recv_right[k * yz + t];
+  }
+}
+
+// In-process variant: read the neighbours' buffers directly (same device or
+// peer-mapped), no staging.
+template <class L, class R, int D>
+__global__ void k_halo_pull(Geom g, R* __restrict__ buf, const R* __restrict__ left, Geom gl,
+                            const R* __restrict__ right, Geom gr) {
+  const long long yz = (long long)g.ny * g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= yz) return;
+#pragma unroll
+  for (int k = 0; k < kHaloPlanes<L>; ++k) {
+    const int pr = halo_slot<L, D, -1>(k), pl = halo_slot<L, D, +1>(k);
+    buf[pr * g.N + (long long)g.nx * t + (g.nx - 1)] =
+        left[pr * gl.N + (long long)gl.nx * t + (gl.x1 - 1)];
+    buf[pl * g.N + (long long)g.nx * t + g.x1] = right[pl * gr.N + (long long)gr.nx * t + gr.x0];
+  }
+}
+
+// ---------------------------------------------------------------------
 // Host-side launchers (one set per build), dispatched by the engine.
 
 
@@ -1108,6 +1179,26 @@ void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void
     else if (field == 0) k_layout<L, R, -1, false><<<grid, bx, 0, st>>>(g, in, out);
     else if (to_ref) k_layout<L, R, +1, true><<<grid, bx, 0, st>>>(g, in, out);
     else k_layout<L, R, +1, false><<<grid, bx, 0, st>>>(g, in, out);
+  });
+}
+void halo(int op, const Geom& g, int dim, int prec, int field, void* buf, void* a, void* b,
+          const void* left, const Geom& gl, const void* right, const Geom& gr, cudaStream_t st) {
+  const long long yz = (long long)g.ny * g.nz;
+  const unsigned nb = unsigned((yz + 127) / 128);
+  LBGPU_LR_DISPATCH(dim, prec, {
+    R* B = static_cast<R*>(buf);
+    if (op == 0) {  // pack into a (left), b (right)
+      if (field == 0) k_halo_pack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
+      else k_halo_pack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
+    } else if (op == 1) {  // unpack from a (left), b (right)
+      if (field == 0) k_halo_unpack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
+      else k_halo_unpack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
+    } else {  // pull from neighbour buffers
+      if (field == 0)
+        k_halo_pull<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)left, gl, (const R*)right, gr);
+      else
+        k_halo_pull<L, R, +1><<<nb, 128, 0, st>>>(g, B, (const R*)left, gl, (const R*)right, gr);
+    }
   });
 }
 void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st) {

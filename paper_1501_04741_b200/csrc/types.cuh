@@ -63,6 +63,9 @@ struct SweepArgs {
   void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
               void* out, cudaStream_t st);                                                 \
   void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
+  void halo(int op, const Geom& g, int dim, int prec, int field, void* buf, void* a, void* b, \
+            const void* left, const Geom& gl, const void* right, const Geom& gr,             \
+            cudaStream_t st);                                                              \
   }
 LBGPU_DECLARE_LAUNCHERS(fast)
 LBGPU_DECLARE_LAUNCHERS(exact)
