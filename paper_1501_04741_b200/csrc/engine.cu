@@ -233,6 +233,7 @@ struct lbgpu_engine {
   // x-slab geometry: nx is the local array extent; owned
   // columns are local 0..span-1 = global x0..x0+span-1.
   int gnx = 0, x0 = 0, span = 0, slab_count = 1, slab_id = 0;
+  bool ghosts = false;  // ghost-column layout (always with >1 slab; one slab on request)
   // halo exchange: 0 none (one slab, periodic wrap), 1 in-process group
   // (neighbour buffers read directly), 2 NCCL (one slab per rank)
   int xmode = 0;
@@ -241,6 +242,8 @@ struct lbgpu_engine {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   void* halo_buf[4] = {nullptr, nullptr, nullptr, nullptr};  // send L, send R, recv L, recv R
+  cudaStream_t st_comm = nullptr;  // halo traffic overlaps the interior columns
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   bool owns_stream = true;
   long long N = 0;
   int device = 0;
@@ -281,6 +284,9 @@ struct lbgpu_engine {
   ~lbgpu_engine() {
     if (!st) return;  // host-only instance (lbgpu_case_tables)
     if (comm) nccl().CommDestroy(comm);
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_halo) cudaEventDestroy(ev_halo);
+    if (st_comm) cudaStreamDestroy(st_comm);
     for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
@@ -317,6 +323,11 @@ struct lbgpu_engine {
       if (slab_count > gnx) throw Fail{LBGPU_E_CONFIG, "more workers than lattice columns"};
       decompose(gnx, slab_count, slab_id, x0, span);
       nx = lbgpu_slab_nxl(span);
+      ghosts = true;
+    } else if (d.slab_id == -1) {  // one slab in ghost layout: a single-rank ring
+      x0 = 0, span = gnx, slab_id = 0;
+      nx = lbgpu_slab_nxl(span);
+      ghosts = true;
     } else {
       x0 = 0, span = gnx;
     }
@@ -563,6 +574,7 @@ struct lbgpu_engine {
     if (resid_slot) s.a.fl.resid = resid_slot;
     s.dim = dim, s.prec = prec, s.ck = ck, s.resid = resid;
     s.adj_side = d_adj_side, s.n_adj_side = (long long)adj_side.size();
+    s.part = 0;
     return s;
   }
   void sync() { CU(cudaStreamSynchronize(st)); }
@@ -591,28 +603,55 @@ struct lbgpu_engine {
   }
 
   // ------------------------------------------------------------ sweeps
+  // NCCL mode: the two boundary columns first, their halo on the comm stream
+  // while the interior columns compute, joined before the next sweep.
+  template <class F>
+  void overlapped(int field, void* dst, SweepArgs s, F&& launch_part) {
+    s.part = 2;
+    launch_part(s);
+    CU(cudaEventRecord(ev_bnd, st));
+    CU(cudaStreamWaitEvent(st_comm, ev_bnd, 0));
+    nccl_exchange(field, dst, st_comm);
+    CU(cudaEventRecord(ev_halo, st_comm));
+    s.part = 1;
+    launch_part(s);
+    CU(cudaStreamWaitEvent(st, ev_halo, 0));
+    launches += 1;
+  }
+
   void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
     ++primal_steps;
     ++launches;
     const SweepArgs s = sweep(primal_steps, resid, slot);
-    if (exact) exact::primal(s, f[fc], f[1 - fc]);
-    else fast::primal(s, f[fc], f[1 - fc]);
+    void* src = f[fc];
+    void* dst = f[1 - fc];
+    auto go = [&](const SweepArgs& a) {
+      if (exact) exact::primal(a, src, dst);
+      else fast::primal(a, src, dst);
+    };
+    if (exch && xmode == 2) overlapped(0, dst, s, go);
+    else go(s);
     fc ^= 1;
-    if (exch && xmode == 2) exchange(0);
   }
   void adjoint_launch(int kernel, bool resid, unsigned long long* slot, bool exch = true) {
     ++adjoint_steps;
     ++launches;
     const SweepArgs s = sweep(adjoint_steps, resid, slot);
-    if (kernel) {
-      if (exact) exact::adjoint_dual(s, f[fc], v[vc], v[1 - vc]);
-      else fast::adjoint_dual(s, f[fc], v[vc], v[1 - vc]);
-    } else {
-      if (exact) exact::adjoint(s, f[fc], v[vc], v[1 - vc]);
-      else fast::adjoint(s, f[fc], v[vc], v[1 - vc]);
-    }
+    void* base = f[fc];
+    void* src = v[vc];
+    void* dst = v[1 - vc];
+    auto go = [&](const SweepArgs& a) {
+      if (kernel) {
+        if (exact) exact::adjoint_dual(a, base, src, dst);
+        else fast::adjoint_dual(a, base, src, dst);
+      } else {
+        if (exact) exact::adjoint(a, base, src, dst);
+        else fast::adjoint(a, base, src, dst);
+      }
+    };
+    if (exch && xmode == 2) overlapped(1, dst, s, go);
+    else go(s);
     vc ^= 1;
-    if (exch && xmode == 2) exchange(1);
   }
 
   // ------------------------------------------------------------ halo
@@ -622,12 +661,15 @@ struct lbgpu_engine {
     for (void*& h : halo_buf)
       if (!h) CU(cudaMalloc(&h, halo_bytes()));
   }
-  void halo_op(int op, int field, void* a, void* b, const lbgpu_engine* l, const lbgpu_engine* r) {
+  void halo_op(int op, int field, void* a, void* b, const lbgpu_engine* l, const lbgpu_engine* r,
+               void* buf = nullptr, cudaStream_t s_ = nullptr) {
     const Geom gl = l ? l->G : G, gr = r ? r->G : G;
     const void* lb = l ? l->cur(field) : nullptr;
     const void* rb = r ? r->cur(field) : nullptr;
-    if (exact) exact::halo(op, G, dim, prec, field, cur(field), a, b, lb, gl, rb, gr, st);
-    else fast::halo(op, G, dim, prec, field, cur(field), a, b, lb, gl, rb, gr, st);
+    void* B = buf ? buf : cur(field);
+    cudaStream_t S = s_ ? s_ : st;
+    if (exact) exact::halo(op, G, dim, prec, field, B, a, b, lb, gl, rb, gr, S);
+    else fast::halo(op, G, dim, prec, field, B, a, b, lb, gl, rb, gr, S);
     ++launches;
   }
   // Fill this slab's ghost columns of `field` after a sweep of it.
@@ -635,8 +677,14 @@ struct lbgpu_engine {
     if (xmode == 1) {
       halo_op(2, field, nullptr, nullptr, nb_left, nb_right);
     } else if (xmode == 2) {
+      nccl_exchange(field, cur(field), st);
+    }
+  }
+  // pack -> NCCL send/recv with both neighbours -> unpack, all on stream S.
+  void nccl_exchange(int field, void* buf, cudaStream_t S) {
+    {
       ensure_halo_bufs();
-      halo_op(0, field, halo_buf[0], halo_buf[1], nullptr, nullptr);
+      halo_op(0, field, halo_buf[0], halo_buf[1], nullptr, nullptr, buf, S);
       const size_t cnt = halo_bytes() / bytes_per_real();
       const ncclDataType_t ty = prec == 64 ? ncclFloat64 : ncclFloat32;
       const int left = (rank - 1 + nranks) % nranks, right = (rank + 1) % nranks;
@@ -644,13 +692,13 @@ struct lbgpu_engine {
       // (left == right) the i-th send meets the i-th receive
       const Nccl& N_ = nccl();
       N_.GroupStart();
-      N_.Send(halo_buf[1], cnt, ty, right, comm, st);
-      N_.Recv(halo_buf[2], cnt, ty, left, comm, st);
-      N_.Send(halo_buf[0], cnt, ty, left, comm, st);
-      N_.Recv(halo_buf[3], cnt, ty, right, comm, st);
+      N_.Send(halo_buf[1], cnt, ty, right, comm, S);
+      N_.Recv(halo_buf[2], cnt, ty, left, comm, S);
+      N_.Send(halo_buf[0], cnt, ty, left, comm, S);
+      N_.Recv(halo_buf[3], cnt, ty, right, comm, S);
       const ncclResult_t r = N_.GroupEnd();
       if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + N_.GetErrorString(r)};
-      halo_op(1, field, halo_buf[2], halo_buf[3], nullptr, nullptr);
+      halo_op(1, field, halo_buf[2], halo_buf[3], nullptr, nullptr, buf, S);
     }
   }
   // Global max / min of device flag words across ranks (NCCL mode).
@@ -991,12 +1039,17 @@ int lbgpu_attach_nccl(lbgpu_engine* e, const void* uid, int nranks, int rank) {
   return guarded(e, [&] {
     if (e->slab_count != nranks || e->slab_id != rank)
       throw Fail{LBGPU_E_CONFIG, "engine must be slab `rank` of `nranks`"};
+    if (nranks == 1 && !e->ghosts)
+      throw Fail{LBGPU_E_CONFIG, "a single-rank ring needs the ghost-column layout (slab_id -1)"};
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     const ncclResult_t r = nccl().CommInitRank(&e->comm, nranks, id, rank);
     if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + nccl().GetErrorString(r)};
     e->rank = rank, e->nranks = nranks;
-    e->xmode = nranks > 1 ? 2 : 0;
+    e->xmode = 2;
+    CU(cudaStreamCreateWithFlags(&e->st_comm, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&e->ev_bnd, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&e->ev_halo, cudaEventDisableTiming));
   });
 }
 
@@ -1037,7 +1090,9 @@ static int desc_from_config(const char* cfg_text, const char* overrides, int dev
     return LBGPU_E_CONFIG;
   }
   bool ok;
-  if (slab_count > 1) {
+  if (slab_count <= 1 && slab_id == -1) {
+    ok = build_slab(c, 0, c.nx, lbgpu_slab_nxl(c.nx), s, err);
+  } else if (slab_count > 1) {
     if (slab_id < 0 || slab_id >= slab_count || slab_count > c.nx) {
       g_create_err = "invalid slab decomposition";
       return LBGPU_E_CONFIG;

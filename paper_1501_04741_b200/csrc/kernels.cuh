@@ -714,24 +714,44 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 // lanes rebuild their inputs in place (face_forward) and share the interior
 // collision with the rest of the warp.
 template <class L, class R, int CK, bool RESID>
-__global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
-                                                R* __restrict__ dst) {
+__device__ __forceinline__ void primal_body(const Launch& a, const R* __restrict__ src,
+                                            R* __restrict__ dst, int x, int y, int z,
+                                            unsigned long long& rmax) {
   using namespace detail;
   const Geom& g = a.g;
-  const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+  const uint8_t code = a.t.code[idx];
+  const Nbr nb = make_nbr(g, x, y, z);
+  R f[L::M], out[L::M];
+  gather<L, R, -1>(src, g.N, nb, f);
+  if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
+    atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+  store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
+}
+
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
+                                                R* __restrict__ dst) {
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
-  if (x < g.x1) {
-    const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
-    const uint8_t code = a.t.code[idx];
-    const Nbr nb = make_nbr(g, x, y, z);
-    R f[L::M], out[L::M];
-    gather<L, R, -1>(src, g.N, nb, f);
-    if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
-      atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
+  if (x < a.g.x1) primal_body<L, R, CK, RESID>(a, src, dst, x, blockIdx.y, blockIdx.z, rmax);
+  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
+}
+
+// The two boundary columns (c0, c1) of a slab, one thread per (column, y, z):
+// computed first so their halo can travel while k_primal does the interior.
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restrict__ src,
+                                                     R* __restrict__ dst, int c0, int c1) {
+  const long long yz = (long long)a.g.ny * a.g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (t < 2 * yz) {
+    const long long r = t % yz;
+    primal_body<L, R, CK, RESID>(a, src, dst, t < yz ? c0 : c1, int(r % a.g.ny),
+                                 int(r / a.g.ny), rmax);
   }
-  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
 // Adjoint sweep (adjoint_step, adjoint.cpp:206-254, in pull form): gathers v
@@ -744,76 +764,98 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
 // the rare side-list nodes (synthetic-objective support, support nodes on a
 // face) to k_adjoint_side.
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
+__device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restrict__ base,
+                                             const R* __restrict__ src, R* __restrict__ dst,
+                                             int x, int y, int z, unsigned long long& rmax) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const long long N = g.N;
+  const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+  const uint8_t code = a.t.code[idx];
+  const int tag = code & TAG_MASK;
+  const bool face = is_face(tag);
+  const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
+  if (!(SPLIT && side)) {
+    const Nbr nb = make_nbr(g, x, y, z);
+    R vin[L::M], vout[L::M];
+    bool ok = true;
+    if (LBGPU_EXACT || AK == 1 || !SPLIT) {
+      R fin[L::M];
+      gather<L, R, -1>(base, N, nb, fin);
+      gather<L, R, +1>(src, N, nb, vin);
+      ok = adjoint_node_full<L, R, CK, AK>(a, idx, code, fin, vin, vout);
+    } else {
+      R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
+      FaceState<R> fs{};
+      const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
+      if (need) {
+        R fin[L::M];
+        gather<L, R, -1>(base, N, nb, fin);
+        if (face) {
+          const bool inlet = tag == TAG_INLET;
+          const double bcT = a.t.bcT[idx];
+          face_dispatch<L>(code, [&]<int AX, int SG>() {
+            fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, fin);
+          });
+        }
+        flow_sums<L, R>(fin, rho, jv);
+#pragma unroll
+        for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
+      }
+      gather<L, R, +1>(src, N, nb, vin);
+      if (tag == TAG_WALL) {
+        LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+      } else if (tag == TAG_HEATER) {
+        LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+#pragma unroll
+        for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
+      } else {
+        const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+        const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
+        const double omt = node_omt<R>(a.M, a.t, code, w);
+        ok = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout,
+                                  vout + L::MF);
+        if (face) {
+          const bool inlet = tag == TAG_INLET;
+          face_dispatch<L>(code, [&]<int AX, int SG>() {
+            face_reverse<L, R, AX, SG>(inlet, fs, vout);
+          });
+        }
+      }
+      if (code & CODE_SUPPORT) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
+    }
+    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
+  }
+  }
+
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
 __global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint(Launch a,
                                                                 const R* __restrict__ base,
                                                                 const R* __restrict__ src,
                                                                 R* __restrict__ dst) {
-  using namespace detail;
-  const Geom& g = a.g;
-  const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
-  if (x < g.x1) {
-    const long long N = g.N;
-    const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
-    const uint8_t code = a.t.code[idx];
-    const int tag = code & TAG_MASK;
-    const bool face = is_face(tag);
-    const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
-    if (!(SPLIT && side)) {
-      const Nbr nb = make_nbr(g, x, y, z);
-      R vin[L::M], vout[L::M];
-      bool ok = true;
-      if (LBGPU_EXACT || AK == 1 || !SPLIT) {
-        R fin[L::M];
-        gather<L, R, -1>(base, N, nb, fin);
-        gather<L, R, +1>(src, N, nb, vin);
-        ok = adjoint_node_full<L, R, CK, AK>(a, idx, code, fin, vin, vout);
-      } else {
-        R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
-        FaceState<R> fs{};
-        const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
-        if (need) {
-          R fin[L::M];
-          gather<L, R, -1>(base, N, nb, fin);
-          if (face) {
-            const bool inlet = tag == TAG_INLET;
-            const double bcT = a.t.bcT[idx];
-            face_dispatch<L>(code, [&]<int AX, int SG>() {
-              fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, fin);
-            });
-          }
-          flow_sums<L, R>(fin, rho, jv);
-#pragma unroll
-          for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
-        }
-        gather<L, R, +1>(src, N, nb, vin);
-        if (tag == TAG_WALL) {
-          LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
-        } else if (tag == TAG_HEATER) {
-          LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
-#pragma unroll
-          for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
-        } else {
-          const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-          const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
-          const double omt = node_omt<R>(a.M, a.t, code, w);
-          ok = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout,
-                                    vout + L::MF);
-          if (face) {
-            const bool inlet = tag == TAG_INLET;
-            face_dispatch<L>(code, [&]<int AX, int SG>() {
-              face_reverse<L, R, AX, SG>(inlet, fs, vout);
-            });
-          }
-        }
-        if (code & CODE_SUPPORT) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
-      }
-      if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-      store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
-    }
+  if (x < a.g.x1)
+    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, x, blockIdx.y, blockIdx.z, rmax);
+  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
+}
+
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
+__global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint_cols(Launch a,
+                                                                     const R* __restrict__ base,
+                                                                     const R* __restrict__ src,
+                                                                     R* __restrict__ dst, int c0,
+                                                                     int c1) {
+  const long long yz = (long long)a.g.ny * a.g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (t < 2 * yz) {
+    const long long r = t % yz;
+    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, t < yz ? c0 : c1,
+                                             int(r % a.g.ny), int(r / a.g.ny), rmax);
   }
-  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
 // Side-list adjoint nodes with the full (reference-form) node update.
@@ -1063,26 +1105,48 @@ __global__ void k_halo_pull(Geom g, R* __restrict__ buf, const R* __restrict__ l
 // Host-side launchers (one set per build), dispatched by the engine.
 
 
+// part: 0 all owned columns, 1 interior columns only (x0+1 .. x1-2),
+// 2 the two boundary columns only (see SweepArgs).
 template <class L, class R, int CK, bool RES>
 void primal_t(const SweepArgs& s, const void* src, void* dst) {
-  const Geom& g = s.a.g;
-  const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
-  dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
-  k_primal<L, R, CK, RES><<<grid, bx, 0, s.a.stream>>>(s.a, static_cast<const R*>(src),
-                                                        static_cast<R*>(dst));
+  const R* in = static_cast<const R*>(src);
+  R* out = static_cast<R*>(dst);
+  Launch a = s.a;
+  if (s.part == 2) {
+    const long long n = 2ll * a.g.ny * a.g.nz;
+    k_primal_cols<L, R, CK, RES><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
+        a, in, out, a.g.x0, a.g.x1 - 1);
+    return;
+  }
+  if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+  if (a.g.x1 <= a.g.x0) return;
+  const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+  dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+  k_primal<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, in, out);
 }
 template <class L, class R, int CK, int AK, bool RES>
 void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst) {
-  const Geom& g = s.a.g;
-  const int bx = (g.x1 - g.x0) >= 128 ? 128 : ((g.x1 - g.x0) >= 64 ? 64 : 32);
-  dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
   const R* b = static_cast<const R*>(base);
   const R* in = static_cast<const R*>(src);
   R* out = static_cast<R*>(dst);
   constexpr bool split = !LBGPU_EXACT && AK == 0;
-  k_adjoint<L, R, CK, AK, RES, split><<<grid, bx, 0, s.a.stream>>>(s.a, b, in, out);
-  if (split && s.n_adj_side > 0)
-    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, s.a.stream>>>(
+  Launch a = s.a;
+  if (s.part == 2) {
+    const long long n = 2ll * a.g.ny * a.g.nz;
+    k_adjoint_cols<L, R, CK, AK, RES, split><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
+        a, b, in, out, a.g.x0, a.g.x1 - 1);
+  } else {
+    if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+    if (a.g.x1 > a.g.x0) {
+      const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+      dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+      k_adjoint<L, R, CK, AK, RES, split><<<grid, bx, 0, a.stream>>>(a, b, in, out);
+    }
+  }
+  // side-list nodes go with the full sweep, or with the boundary part so that
+  // they are final before a halo is packed
+  if (split && s.n_adj_side > 0 && s.part != 1)
+    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
         s.a, b, in, out, s.adj_side, s.n_adj_side);
 }
 

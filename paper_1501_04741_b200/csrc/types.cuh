@@ -45,6 +45,7 @@ struct SweepArgs {
   bool resid;
   const long long* adj_side;  // adjoint side-list nodes (k_adjoint_side)
   long long n_adj_side;
+  int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).

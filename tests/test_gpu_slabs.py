@@ -46,3 +46,35 @@ def test_slab_upload_round_trip(lbgpu, has_gpu):
     mono.primal_step(4)
     grp.step(0, 4)
     assert np.array_equal(grp.get_state(0), mono.get_state(0))
+
+
+@pytest.mark.parametrize("name", ["grad2d", "mix3d", "exch3d"])
+def test_nccl_single_rank_ring_equals_monolithic(lbgpu, has_gpu, name):
+    """The NCCL transport (pack -> ncclSend/ncclRecv -> unpack on a comm
+    stream, boundary columns first, interior overlapped) exercised on one GPU:
+    one slab in ghost layout whose left and right neighbour is itself. Must
+    equal the monolithic periodic-wrap run bit for bit, for both sweeps and
+    for the batched tol-stop solver with its cross-rank flag reductions."""
+    import torch  # noqa: F401  (loads torch's libnccl first, as in bench.py)
+    txt = case_text(name)
+    mono = lbgpu.Engine.from_config(txt)
+    ring = lbgpu.Engine.slab_from_config(txt, None, 1, -1)
+    ring.attach_nccl(lbgpu.nccl_unique_id(), 1, 0)
+    s = ring.slab()
+    assert s["nxl"] > s["span"] == s["gnx"]
+    mono.init_state()
+    ring.init_state()
+
+    def owned(e, field):
+        nx, ny, nz = mono.shape
+        return e.get_state(field).reshape(e.m, nz, ny, s["nxl"])[..., : s["span"]].reshape(-1)
+
+    assert mono.primal_step(25) == ring.primal_step(25)
+    assert np.array_equal(owned(ring, 0), mono.get_state(0))
+    assert mono.adjoint_step(9) == ring.adjoint_step(9)
+    assert np.array_equal(owned(ring, 1), mono.get_state(1))
+    g_m, d_m = mono.param_gradient()
+    g_r, d_r = ring.param_gradient()
+    assert np.array_equal(g_m, g_r) and d_m == d_r
+    assert mono.solve_primal(1e-6, 20000) == ring.solve_primal(1e-6, 20000)
+    assert np.array_equal(owned(ring, 0), mono.get_state(0))
