@@ -168,6 +168,19 @@ int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta,
                    const double* lambda, int64_t record_interval, lbgpu_run_row* rows,
                    int64_t cap, int64_t* n_rows);
 
+/* --- unsteady adjoint (no reference function) --- */
+/* Discrete adjoint of n_steps primal steps from the current state f^0, for
+ * J = F(f^N) (sum_objective = 0) or J = sum_{n=1..N} F(f^n): returns J,
+ * dJ/dw in DesignField::nodes order and dJ/d(inlet_dp). Primal states are
+ * recomputed from checkpoints by recursive bisection within `slots` device
+ * state buffers; forward_sweeps reports the primal sweeps spent (>= N).
+ * Leaves f^N as the primal state. Equals the composition of the reference's
+ * own adjoint_step / param_gradient (tests/test_gpu_unsteady.py) and
+ * fd_gradient(fixed_iters = N). */
+int lbgpu_unsteady_adjoint(lbgpu_engine* e, int64_t n_steps, int sum_objective, int64_t slots,
+                           double* g_design, double* g_inlet_dp, double* J,
+                           int64_t* forward_sweeps);
+
 /* --- multi-slab runs (PartitionedRun, partition.cpp:43-312) --- */
 /* In-process group: engines[i] must be slab i of n (same device); they then
  * share one stream and step in lock step through the lbgpu_group_* calls,

@@ -122,6 +122,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_nccl_unique_id.argtypes = [vp, C.c_int]
     L.lbgpu_attach_nccl.argtypes = [vp, vp, C.c_int, C.c_int]
     L.lbgpu_exchange.argtypes = [vp, C.c_int]
+    L.lbgpu_unsteady_adjoint.argtypes = [vp, i64, C.c_int, i64, vp, dp, dp, C.POINTER(i64)]
     L.lbgpu_sweep_launches.argtypes = [vp]
     L.lbgpu_sweep_launches.restype = i64
     _lib = L
@@ -335,6 +336,16 @@ class Engine:
         self._ok(self.L.lbgpu_one_shot(self.h, iters, _ptr(zeta), _ptr(lam), record_interval,
                                        C.addressof(rows), cap, C.byref(nr)))
         return np.array([[getattr(r, k) for k, _ in RunRow._fields_] for r in rows[: nr.value]])
+
+    def unsteady_adjoint(self, n_steps: int, sum_objective: bool = False, slots: int = 8):
+        """Discrete adjoint of n_steps primal steps from the current state
+        (checkpoint + recompute). Returns (J, dJ/dw design order, dJ/d inlet_dp,
+        primal sweeps spent)."""
+        g = np.zeros(max(self.n_design, 1))
+        gdp, J, fs = C.c_double(), C.c_double(), C.c_int64()
+        self._ok(self.L.lbgpu_unsteady_adjoint(self.h, n_steps, int(sum_objective), slots, _ptr(g),
+                                               C.byref(gdp), C.byref(J), C.byref(fs)))
+        return J.value, g[: self.n_design], gdp.value, fs.value
 
     def time_sweeps(self, which: int, steps: int) -> float:
         """Milliseconds of `steps` back-to-back sweeps (CUDA events on the

@@ -363,6 +363,7 @@ struct lbgpu_engine {
       if (tag[i] == TAG_INLET && owned) inlets.push_back(i);
     }
     M.obj_kind = d.obj_kind, M.flux_axis = d.flux_axis, M.flux_sign = d.flux_sign;
+    M.obj_on = 1;
     if (d.obj_kind < 0 || d.obj_kind > 2) throw Fail{LBGPU_E_CONFIG, "unknown objective kind"};
     if (d.n_support > 0) support.assign(d.support, d.support + d.n_support);
     for (size_t k = 0; k < support.size(); ++k)
@@ -619,27 +620,24 @@ struct lbgpu_engine {
     launches += 1;
   }
 
-  void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
+  // One primal sweep src -> dst (and, in NCCL mode, the halo of dst).
+  void primal_raw(const void* src, void* dst, bool resid, unsigned long long* slot, bool exch) {
     ++primal_steps;
     ++launches;
     const SweepArgs s = sweep(primal_steps, resid, slot);
-    void* src = f[fc];
-    void* dst = f[1 - fc];
     auto go = [&](const SweepArgs& a) {
       if (exact) exact::primal(a, src, dst);
       else fast::primal(a, src, dst);
     };
     if (exch && xmode == 2) overlapped(0, dst, s, go);
     else go(s);
-    fc ^= 1;
   }
-  void adjoint_launch(int kernel, bool resid, unsigned long long* slot, bool exch = true) {
+  // One adjoint sweep src -> dst against the primal pull buffer `base`.
+  void adjoint_raw(int kernel, const void* base, const void* src, void* dst, bool resid,
+                   unsigned long long* slot, bool exch) {
     ++adjoint_steps;
     ++launches;
     const SweepArgs s = sweep(adjoint_steps, resid, slot);
-    void* base = f[fc];
-    void* src = v[vc];
-    void* dst = v[1 - vc];
     auto go = [&](const SweepArgs& a) {
       if (kernel) {
         if (exact) exact::adjoint_dual(a, base, src, dst);
@@ -651,6 +649,13 @@ struct lbgpu_engine {
     };
     if (exch && xmode == 2) overlapped(1, dst, s, go);
     else go(s);
+  }
+  void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
+    primal_raw(f[fc], f[1 - fc], resid, slot, exch);
+    fc ^= 1;
+  }
+  void adjoint_launch(int kernel, bool resid, unsigned long long* slot, bool exch = true) {
+    adjoint_raw(kernel, f[fc], v[vc], v[1 - vc], resid, slot, exch);
     vc ^= 1;
   }
 
@@ -827,11 +832,11 @@ struct lbgpu_engine {
     sync();
     return out;
   }
-  double objective() {
-    reset_flags();
+  double objective(const void* buf = nullptr) {
     const Launch a = launch(primal_steps);
-    if (exact) exact::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms);
-    else fast::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms);
+    const void* P = buf ? buf : f[fc];
+    if (exact) exact::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms);
+    else fast::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms);
     CU(cudaGetLastError());
     const double val = pairwise(tree_support, d_terms);
     check_bad("iteration");
@@ -847,8 +852,8 @@ struct lbgpu_engine {
     reset_flags();
     const Launch a = launch(adjoint_steps);
     const long long n = (long long)design.size();
-    if (exact) exact::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0);
-    else fast::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0);
+    if (exact) exact::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0);
+    else fast::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0);
     CU(cudaGetLastError());
     if (g && n) CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     if (gdp) {
@@ -859,6 +864,143 @@ struct lbgpu_engine {
       *gdp = pairwise(tree_inlet, d_terms);
     }
     check_bad("gradient at iteration");
+  }
+
+  // ------------------------------------------------- unsteady adjoint
+  // Discrete adjoint of N primal steps (no reference
+  // function — SPEC.md:313). With P = S o W one primal step, the reference's
+  // adjoint_step(base b, v) = S^-1 (J_W(b)^T v + dF(b)):
+  //   mu^N     = adjoint_step(base f^N, 0, obj)
+  //   mu^{n-1} = adjoint_step(base f^{n-1}, mu^n, obj if sum else none)
+  //   dJ/dw    = sum_{n=N..1} param_gradient(v = mu^n, base f^{n-1})
+  // for J = F(f^N) (terminal) or J = sum_{n=1..N} F(f^n). Primal states are
+  // recomputed from checkpoints by recursive bisection over `slots` state
+  // buffers (O(N log(N/slots)) extra sweeps, O(slots) memory); the sweeps
+  // write straight into the slot buffers (no copies).
+  struct Unsteady {
+    lbgpu_engine* e;
+    bool sum;
+    std::vector<void*> free_slots;
+    void* work;   // ping-pong partners for forward segments
+    void* work2;
+    double gdp = 0.0;
+    // k >= 1 sweeps from `from`, the last one landing in `to` (via `tmp`)
+    void fwd(const void* from, void* to, long long k, void* tmp) {
+      const void* src = from;
+      for (long long i = 0; i < k; ++i) {
+        void* dst = ((k - 1 - i) % 2 == 0) ? to : tmp;
+        e->primal_raw(src, dst, false, nullptr, true);
+        src = dst;
+      }
+    }
+    // mu^n -> grad += g(mu^n, f^{n-1}); mu^{n-1} = adjoint(f^{n-1}, mu^n)
+    void back_step(const void* base) {
+      const long long nd = (long long)e->design.size();
+      const Launch a = e->launch(e->adjoint_steps);
+      if (e->exact) exact::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1);
+      else fast::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1);
+      if (!e->inlets.empty()) {
+        if (e->exact) exact::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms);
+        else fast::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms);
+        gdp += e->pairwise(e->tree_inlet, e->d_terms);
+      }
+      e->M.obj_on = sum ? 1 : 0;
+      e->adjoint_raw(0, base, e->v[e->vc], e->v[1 - e->vc], false, nullptr, true);
+      e->vc ^= 1;
+      e->M.obj_on = 1;
+    }
+    // On entry v holds mu^b and `A` holds state a; leaves mu^a in v.
+    void reverse(long long a, long long b, const void* A) {
+      const long long inner = b - a - 1;  // states a+1 .. b-1
+      if (inner > 0 && free_slots.empty()) {  // no memory left: recompute each base from A
+        for (long long n = b; n > a; --n) {
+          if (n - 1 == a) {
+            back_step(A);
+          } else {
+            fwd(A, work2, n - 1 - a, work);
+            back_step(work2);
+          }
+        }
+        return;
+      }
+      if (inner <= (long long)free_slots.size()) {
+        std::vector<void*> st(inner);
+        const void* prev = A;
+        for (long long k = 0; k < inner; ++k) {
+          st[k] = free_slots.back();
+          free_slots.pop_back();
+          e->primal_raw(prev, st[k], false, nullptr, true);
+          prev = st[k];
+        }
+        for (long long n = b; n > a; --n) back_step(n - 1 == a ? A : st[n - 1 - a - 1]);
+        for (void* p : st) free_slots.push_back(p);
+        return;
+      }
+      const long long m = a + (b - a) / 2;
+      void* Ms = free_slots.back();
+      free_slots.pop_back();
+      fwd(A, Ms, m - a, work);
+      reverse(m, b, Ms);
+      free_slots.push_back(Ms);
+      reverse(a, m, A);
+    }
+  };
+
+  void unsteady(long long N, bool sum_obj, long long max_slots, double* g, double* gdp, double* J,
+                long long* fsteps) {
+    require_solo();
+    if (N < 1) throw Fail{LBGPU_E_ARG, "unsteady adjoint needs at least one step"};
+    const long long nslots = std::max<long long>(1, std::min<long long>(max_slots, N));
+    std::vector<void*> slots;
+    auto release = [&] {
+      for (void* p : slots) cudaFree(p);
+    };
+    try {
+      for (long long i = 0; i < nslots + 3; ++i) {
+        void* p = nullptr;
+        CU(cudaMalloc(&p, field_bytes()));
+        slots.push_back(p);
+      }
+      void* s0 = slots[0];     // state 0 (checkpoint)
+      void* work = slots[1];   // forward ping-pong partner
+      void* sN = slots[2];     // state N during the first pass
+      const long long steps0 = primal_steps;
+      reset_flags();
+      CU(cudaMemcpyAsync(s0, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
+      // first pass: states 1..N, the objective
+      double Jv = 0.0;
+      const void* src = s0;
+      for (long long n = 1; n <= N; ++n) {
+        void* dst = (n % 2 == N % 2) ? sN : work;
+        primal_raw(src, dst, false, nullptr, true);
+        src = dst;
+        if (sum_obj || n == N) Jv += objective(dst);
+      }
+      // mu^N = adjoint_step(f^N, 0, obj)
+      CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
+      CU(cudaMemsetAsync(v[1 - vc], 0, field_bytes(), st));
+      CU(cudaMemsetAsync(d_grad, 0, sizeof(double) * std::max<size_t>(design.size(), 1), st));
+      adjoint_raw(0, sN, v[vc], v[1 - vc], false, nullptr, true);
+      vc ^= 1;
+      // keep f^N as the engine's primal state afterwards
+      CU(cudaMemcpyAsync(f[fc], sN, field_bytes(), cudaMemcpyDeviceToDevice, st));
+      Unsteady U{this, sum_obj, {}, work, slots[3]};
+      for (long long i = 4; i < (long long)slots.size(); ++i) U.free_slots.push_back(slots[i]);
+      U.free_slots.push_back(sN);
+      U.reverse(0, N, s0);
+      if (g && !design.empty())
+        CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * design.size(), cudaMemcpyDeviceToHost, st));
+      sync();
+      check_bad("unsteady iteration");
+      if (gdp) *gdp = U.gdp;
+      if (J) *J = Jv;
+      if (fsteps) *fsteps = primal_steps - steps0;
+    } catch (...) {
+      sync();
+      release();
+      throw;
+    }
+    release();
   }
 
   void one_shot(long long iters, const double* zeta, const double* lambda, long long ri,
@@ -874,8 +1016,8 @@ struct lbgpu_engine {
       adjoint_launch(0, false, nullptr);
       if (rec) CU(cudaMemsetAsync(d_flags + 2, 0, sizeof(unsigned long long), st));
       const Launch a = launch(adjoint_steps);
-      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1]);
-      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1]);
+      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1], 0);
+      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1], 0);
       CU(cudaGetLastError());
       if (exact) {  // the device moved w: refresh the host copy and the libm pow tables
         CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
@@ -1395,6 +1537,17 @@ int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
     CU(cudaEventElapsedTime(&t, e->ev0, e->ev1));
     *ms = t;
     e->check_bad(which == 0 ? "iteration" : "adjoint iteration");
+  });
+}
+
+int lbgpu_unsteady_adjoint(lbgpu_engine* e, int64_t n_steps, int sum_objective, int64_t slots,
+                           double* g_design, double* g_inlet_dp, double* J,
+                           int64_t* forward_sweeps) {
+  if (n_steps < 1 || slots < 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long fs = 0;
+    e->unsteady(n_steps, sum_objective != 0, slots, g_design, g_inlet_dp, J, &fs);
+    if (forward_sweeps) *forward_sweeps = fs;
   });
 }
 

@@ -691,7 +691,7 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 #endif
     }
   }
-  if (code & CODE_SUPPORT) {
+  if (a.M.obj_on && (code & CODE_SUPPORT)) {
     R b[L::M];
     if (node_partial<L, R>(a.M, fin, b)) {
 #pragma unroll
@@ -822,7 +822,7 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
           });
         }
       }
-      if (code & CODE_SUPPORT) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
+      if (a.M.obj_on && (code & CODE_SUPPORT)) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
     }
     if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
     store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
                                                   const long long* __restrict__ nodes,
                                                   long long n, double* __restrict__ gout,
                                                   double* __restrict__ w_rw, double zeta,
-                                                  double lambda) {
+                                                  double lambda, int accumulate) {
   using namespace detail;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long cmax = 0;
@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
       w_rw[idx] = wn;
       cmax = (unsigned long long)__double_as_longlong(fabs(comp));
     } else {
-      gout[i] = gv;
+      gout[i] = accumulate ? gout[i] + gv : gv;
     }
   }
   if constexpr (UPDATE) block_max_bits(cmax, a.fl.aux);
@@ -1204,17 +1204,17 @@ void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* d
 #if defined(LBGPU_PART_AUX)
 void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,
               const void* q, const long long* nodes, long long n, double* gout, double* w_rw,
-              double zeta, double lambda) {
+              double zeta, double lambda, int accumulate) {
   if (n <= 0) return;
   const int bs = 128;
   const unsigned nb = unsigned((n + bs - 1) / bs);
   LBGPU_LR_DISPATCH(dim, prec, {
     const R* pp = static_cast<const R*>(p);
     const R* qq = static_cast<const R*>(q);
-    if (ak == 0 && !update) k_gradient<L, R, 0, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
-    else if (ak == 0) k_gradient<L, R, 0, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
-    else if (!update) k_gradient<L, R, 1, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
-    else k_gradient<L, R, 1, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda);
+    if (ak == 0 && !update) k_gradient<L, R, 0, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    else if (ak == 0) k_gradient<L, R, 0, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    else if (!update) k_gradient<L, R, 1, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    else k_gradient<L, R, 1, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
   });
 }
 void objective_terms(const Launch& a, int dim, int prec, const void* p, const long long* nodes,

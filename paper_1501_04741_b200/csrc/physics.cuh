@@ -74,6 +74,7 @@ struct Model {
   const double* A;    // dense relaxation matrix (mf x mf), reference order
   const double* At;   // its transpose (ModelTables::At)
   int obj_kind;       // 0 mixing 1 heatflux 2 synthetic
+  int obj_on;         // adjoint sweeps add the objective partial on support nodes
   int flux_axis, flux_sign;
 };
 

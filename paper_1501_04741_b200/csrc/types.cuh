@@ -56,7 +56,7 @@ struct SweepArgs {
   void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* dst);     \
   void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,    \
                 const void* q, const long long* nodes, long long n, double* gout,          \
-                double* w_rw, double zeta, double lambda);                                 \
+                double* w_rw, double zeta, double lambda, int accumulate);                 \
   void objective_terms(const Launch& a, int dim, int prec, const void* p,                  \
                        const long long* nodes, long long n, double* terms);                \
   void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,       \
