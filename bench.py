@@ -243,17 +243,18 @@ def main() -> None:
         traffic = tj.get("adjoint_bytes_per_launch")
 
     # e2e through the public C ABI with host buffers: each step uploads the
-    # design field from pinned host memory (lbgpu_set_design, the host-driven
-    # design loop's input) and runs one primal and one adjoint sweep, each
-    # returning its step residual to the host (lbgpu_primal_step /
+    # design vector (DesignField::nodes order, as a host-side optimizer such as
+    # the reference's MMA update produces it) from pinned host memory
+    # (lbgpu_set_design_values) and runs one primal and one adjoint sweep,
+    # each returning its step residual to the host (lbgpu_primal_step /
     # lbgpu_adjoint_step).
-    w_host = torch.from_numpy(eng.design()).pin_memory()
+    w_host = torch.from_numpy(eng.design_values()).pin_memory()
     w_np = w_host.numpy()
-    eng.set_design(w_np)
+    eng.set_design_values(w_np)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        eng.set_design(w_np)
+        eng.set_design_values(w_np)
         eng.primal_step(1)
         eng.adjoint_step(1)
     torch.cuda.synchronize(local)
@@ -263,9 +264,10 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
     e2e = {"value": world * nodes * args.e2e_steps / e2e_s / 1e6, "unit": "MLUPS",
-           "h2d_bytes_per_step": int(nodes * 9), "d2h_bytes_per_step": 16,
+           "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": 16,
            "steps": args.e2e_steps,
-           "path": "lbgpu_set_design(pinned host w) + lbgpu_primal_step + lbgpu_adjoint_step"}
+           "path": "lbgpu_set_design_values(pinned host w) + lbgpu_primal_step + "
+                   "lbgpu_adjoint_step (each returns its residual)"}
 
     if rank != 0:
         if dist:

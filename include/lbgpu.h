@@ -136,6 +136,10 @@ int lbgpu_upload_state_device(lbgpu_engine* e, int field, const double* d_ref_la
 int lbgpu_download_state_device(lbgpu_engine* e, int field, double* d_ref_layout);
 int lbgpu_set_design(lbgpu_engine* e, const double* w_full);   /* DesignField::w (N) */
 int lbgpu_get_design(const lbgpu_engine* e, double* w_full);
+/* The design vector in DesignField::nodes order (n_design values): the form
+ * descent_update / mma_update produce (optimizer.cpp:8-16, :105-138). */
+int lbgpu_set_design_values(lbgpu_engine* e, const double* w_design);
+int lbgpu_get_design_values(lbgpu_engine* e, double* w_design);
 
 /* --- sweeps --- */
 /* n x primal_step (collision.cpp:308-363); residual (nullable) = step_residual

@@ -100,6 +100,8 @@ def load_library() -> C.CDLL:
         getattr(L, name).argtypes = [vp, C.c_int, vp]
     L.lbgpu_set_design.argtypes = [vp, vp]
     L.lbgpu_get_design.argtypes = [vp, vp]
+    L.lbgpu_set_design_values.argtypes = [vp, vp]
+    L.lbgpu_get_design_values.argtypes = [vp, vp]
     L.lbgpu_primal_step.argtypes = [vp, i64, dp]
     L.lbgpu_adjoint_step.argtypes = [vp, i64, C.c_int, dp]
     L.lbgpu_solve_primal.argtypes = [vp, C.c_double, i64, i64, C.POINTER(i64), dp,
@@ -280,6 +282,17 @@ class Engine:
     def set_design(self, w_full: np.ndarray) -> None:
         w_full = np.ascontiguousarray(w_full, np.float64)
         self._ok(self.L.lbgpu_set_design(self.h, _ptr(w_full)))
+
+    def set_design_values(self, w_design: np.ndarray) -> None:
+        """Design values in DesignField::nodes order (host buffer, may be pinned)."""
+        w_design = np.ascontiguousarray(w_design, np.float64)
+        assert w_design.size == self.n_design
+        self._ok(self.L.lbgpu_set_design_values(self.h, _ptr(w_design)))
+
+    def design_values(self) -> np.ndarray:
+        out = np.empty(max(self.n_design, 1))
+        self._ok(self.L.lbgpu_get_design_values(self.h, _ptr(out)))
+        return out[: self.n_design]
 
     def design(self) -> np.ndarray:
         out = np.empty(self.n)

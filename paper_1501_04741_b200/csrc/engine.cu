@@ -214,6 +214,12 @@ __global__ void k_combine(double* vals, const int2* ops, int leaves, int nops, d
   *out = nops ? vals[leaves + nops - 1] : vals[0];
 }
 
+__global__ void k_scatter_design(const double* __restrict__ vals, const long long* __restrict__ nodes,
+                                 long long n, double* __restrict__ w) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) w[nodes[i]] = vals[i];
+}
+
 __global__ void k_penalty_terms(const double* __restrict__ w, const long long* __restrict__ nodes,
                                 long long n, double* __restrict__ t) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -267,6 +273,8 @@ struct lbgpu_engine {
   long long* d_adj_side = nullptr;
   double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
   double* d_ref = nullptr;
+  double* d_wvals = nullptr;  // staging for design-order uploads
+  bool w_host_stale = false;  // device w moved ahead of the host copy
   unsigned long long* d_flags = nullptr;  // [resid, bad, aux]
   unsigned long long* d_ring = nullptr;   // per-step residual ring for batched solves
   unsigned long long* h_flags = nullptr;  // pinned mirror
@@ -292,7 +300,7 @@ struct lbgpu_engine {
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
-    cudaFree(d_adj_side);
+    cudaFree(d_adj_side), cudaFree(d_wvals);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -1043,7 +1051,7 @@ struct lbgpu_engine {
         ++k;
       }
     }
-    if (!exact) CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (!exact) w_host_stale = true;
     sync();
     check_bad("iteration");
     *nrows = k;
@@ -1446,6 +1454,7 @@ int lbgpu_set_design(lbgpu_engine* e, const double* w_full) {
   if (!w_full) return LBGPU_E_ARG;
   return guarded(e, [&] {
     e->w.assign(w_full, w_full + e->N);
+    e->w_host_stale = false;
     e->build_codes();
     CU(cudaMemcpyAsync(e->d_w, e->w.data(), sizeof(double) * e->N, cudaMemcpyHostToDevice, e->st));
     CU(cudaMemcpyAsync(e->d_code, e->code.data(), e->N, cudaMemcpyHostToDevice, e->st));
@@ -1456,8 +1465,47 @@ int lbgpu_set_design(lbgpu_engine* e, const double* w_full) {
 
 int lbgpu_get_design(const lbgpu_engine* e, double* w_full) {
   if (!e || !w_full) return LBGPU_E_ARG;
-  std::memcpy(w_full, e->w.data(), sizeof(double) * e->N);
-  return LBGPU_OK;
+  auto* m = const_cast<lbgpu_engine*>(e);
+  return guarded(m, [&] {
+    if (m->w_host_stale) {
+      CU(cudaMemcpyAsync(m->w.data(), m->d_w, sizeof(double) * m->N, cudaMemcpyDeviceToHost, m->st));
+      m->sync();
+      m->w_host_stale = false;
+    }
+    std::memcpy(w_full, m->w.data(), sizeof(double) * m->N);
+  });
+}
+
+int lbgpu_set_design_values(lbgpu_engine* e, const double* w_design) {
+  if (!w_design) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    const long long n = (long long)e->design.size();
+    if (!n) return;
+    if (!e->d_wvals) CU(cudaMalloc(&e->d_wvals, sizeof(double) * n));
+    CU(cudaMemcpyAsync(e->d_wvals, w_design, sizeof(double) * n, cudaMemcpyHostToDevice, e->st));
+    k_scatter_design<<<unsigned((n + 255) / 256), 256, 0, e->st>>>(e->d_wvals, e->d_design, n, e->d_w);
+    CU(cudaGetLastError());
+    if (e->exact) {  // the libm pow tables follow the host copy
+      for (long long i = 0; i < n; ++i) e->w[e->design[i]] = w_design[i];
+      e->refresh_pow_tables();
+    } else {
+      e->w_host_stale = true;
+      e->sync();
+    }
+  });
+}
+
+int lbgpu_get_design_values(lbgpu_engine* e, double* w_design) {
+  if (!w_design) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    std::vector<double> full(e->N);
+    if (e->w_host_stale) {
+      CU(cudaMemcpyAsync(e->w.data(), e->d_w, sizeof(double) * e->N, cudaMemcpyDeviceToHost, e->st));
+      e->sync();
+      e->w_host_stale = false;
+    }
+    for (size_t i = 0; i < e->design.size(); ++i) w_design[i] = e->w[e->design[i]];
+  });
 }
 
 int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual) {
