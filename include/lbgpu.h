@@ -156,6 +156,10 @@ int lbgpu_solve_primal(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fi
 int lbgpu_solve_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed_iters,
                         int kernel, int64_t* iterations, double* residual, int* converged);
 
+/* As lbgpu_solve_adjoint but continuing from the current v (no reset). */
+int lbgpu_continue_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed_iters,
+                           int kernel, int64_t* iterations, double* residual, int* converged);
+
 /* --- reductions --- */
 /* param_gradient (adjoint.cpp:377-420): g_design in DesignField::nodes
  * order (n_design), plus the inlet_dp global (nullable). */
@@ -203,6 +207,13 @@ int lbgpu_nccl_unique_id(void* out, int cap);
 int lbgpu_attach_nccl(lbgpu_engine* e, const void* unique_id, int nranks, int rank);
 /* Exchange the halos of `field` (collective in NCCL mode; after uploads). */
 int lbgpu_exchange(lbgpu_engine* e, int field);
+
+/* Iterations first .. first+count-1 of a one-shot run of `total`
+ * iterations (zeta/lambda indexed from `first`); rows at it % record_interval
+ * == 0 and at it == total. Lets a driver take snapshots between ranges. */
+int lbgpu_one_shot_range(lbgpu_engine* e, int64_t first, int64_t count, int64_t total,
+                         const double* zeta, const double* lambda, int64_t record_interval,
+                         lbgpu_run_row* rows, int64_t cap, int64_t* n_rows);
 
 /* --- timing (device events on the engine stream; bench support) --- */
 /* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of

@@ -37,12 +37,15 @@ def _compile(src: str, hdr_mtime: float, verbose: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON]
-    if os.path.basename(src).startswith("k_exact_"):
-        cmd.append("-fmad=false")
-    if src.endswith(".cpp"):
-        cmd += ["-x", "cu"]
-    cmd += ["-c", src, "-o", obj]
+    if src.endswith(".cpp"):  # host-only C++ (no device code): the host compiler
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
+        cmd = [cxx, "-std=c++20", "-O2", "-fPIC",
+               f"-I{os.path.join(os.path.dirname(HERE), 'include')}", "-c", src, "-o", obj]
+    else:
+        cmd = [NVCC, *ARCH, *COMMON]
+        if os.path.basename(src).startswith("k_exact_"):
+            cmd.append("-fmad=false")
+        cmd += ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

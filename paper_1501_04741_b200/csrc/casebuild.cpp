@@ -141,6 +141,8 @@ void validate_case(const CaseSpec& c);
 
 }  // namespace
 
+bool zeta_stages(const CaseSpec& c, std::vector<std::pair<long, double>>& st, std::string& err);
+
 bool parse_case(const std::string& text, const std::string& overrides, CaseSpec& c,
                 std::string& err) {
   try {
@@ -232,6 +234,11 @@ void validate_case(const CaseSpec& c) {
   if (c.iterations < 0) bad("iterations must be non-negative");
   if (c.outer_iterations < 0) bad("outer_iterations must be non-negative");
   if (c.zeta < 0) bad("zeta must be non-negative");
+  {
+    std::vector<std::pair<long, double>> st;
+    std::string zerr;
+    if (!zeta_stages(c, st, zerr)) bad(zerr);
+  }
   if (c.initial_w < 0 || c.initial_w > 1) bad("initial_w must lie in [0,1]");
   if (c.init_noise < 0) bad("init_noise must be non-negative");
   if (!(c.primal_tol > 0) || !(c.adjoint_tol > 0)) bad("tolerances must be positive");
@@ -247,6 +254,131 @@ void validate_case(const CaseSpec& c) {
   if (c.workers < 1) bad("workers must be at least 1");
 }
 }  // namespace
+
+bool set_case_key(CaseSpec& c, const std::string& dotted, const std::string& value,
+                  std::string& err) {
+  try {
+    const auto dot = dotted.find('.');
+    if (dot == std::string::npos)
+      throw CfgError{"override key must look like section.key: '" + dotted + "'"};
+    apply(c, dotted.substr(0, dot), dotted.substr(dot + 1), value, "<override>", 0);
+    return true;
+  } catch (const CfgError& e) {
+    err = e.msg;
+    return false;
+  }
+}
+
+bool check_case(const CaseSpec& c, std::string& err) {
+  try {
+    validate_case(c);
+    return true;
+  } catch (const CfgError& e) {
+    err = e.msg;
+    return false;
+  }
+}
+
+bool parse_case_text(const std::string& text, const std::string& origin, CaseSpec& c,
+                     std::string& err) {
+  try {
+    c = CaseSpec{};
+    std::istringstream in(text);
+    std::string raw, section;
+    int line = 0;
+    while (std::getline(in, raw)) {
+      ++line;
+      const auto hash = raw.find('#');
+      if (hash != std::string::npos) raw.erase(hash);
+      const std::string s = trim(raw);
+      if (s.empty()) continue;
+      if (s.front() == '[') {
+        if (s.back() != ']') fail(origin, line, "malformed section header '" + s + "'");
+        section = trim(s.substr(1, s.size() - 2));
+        continue;
+      }
+      const auto eq = s.find('=');
+      if (eq == std::string::npos) fail(origin, line, "expected key = value, got '" + s + "'");
+      const std::string key = trim(s.substr(0, eq));
+      const std::string val = trim(s.substr(eq + 1));
+      if (key.empty()) fail(origin, line, "empty key");
+      if (section.empty()) fail(origin, line, "key '" + key + "' appears before any section");
+      apply(c, section, key, val, origin, line);
+    }
+    return true;
+  } catch (const CfgError& e) {
+    err = e.msg;
+    return false;
+  }
+}
+
+// CaseConfig::serialize (config.cpp:172-229): every key in canonical order,
+// doubles in shortest round-trip form.
+std::string serialize_case(const CaseSpec& c) {
+  auto D = [](double v) {
+    char buf[64];
+    const auto r = std::to_chars(buf, buf + sizeof buf, v);
+    return std::string(buf, r.ptr);
+  };
+  std::ostringstream o;
+  o << "[lattice]\nnx = " << c.nx << "\nny = " << c.ny << "\nnz = " << c.nz << "\n";
+  o << "\n[model]\nnu = " << D(c.nu) << "\nbeta_fluid = " << D(c.beta_fluid)
+    << "\nbeta_solid = " << D(c.beta_solid) << "\ninlet_dp = " << D(c.inlet_dp)
+    << "\nu_clamp = " << D(c.u_clamp) << "\ncollision = " << c.collision
+    << "\nprecision = " << c.precision << "\nomega_nonhydro = " << D(c.omega_nonhydro)
+    << "\nswitch_theta = " << D(c.switch_theta) << "\nswitch_form = " << c.switch_form << "\n";
+  o << "\n[tags]\ngeometry = " << c.geometry << "\ndesign_x0 = " << c.design_x0
+    << "\ndesign_x1 = " << c.design_x1 << "\nheater_x0 = " << c.heater_x0
+    << "\nheater_x1 = " << c.heater_x1 << "\ninlet_profile = " << c.inlet_profile
+    << "\ninlet_T = " << D(c.inlet_T) << "\n";
+  o << "\n[objective]\nkind = " << c.objective << "\nplane_offset = " << c.plane_offset
+    << "\npenalty_w0 = " << D(c.penalty_w0) << "\npenalty_growth = " << D(c.penalty_growth)
+    << "\npenalty_interval = " << c.penalty_interval << "\npenalty_start = " << c.penalty_start
+    << "\npenalty_cap = " << D(c.penalty_cap) << "\n";
+  o << "\n[optimizer]\nmethod = " << c.method << "\niterations = " << c.iterations
+    << "\nouter_iterations = " << c.outer_iterations << "\nzeta = " << D(c.zeta)
+    << "\nzeta_stages = " << c.zeta_stages << "\ninitial_w = " << D(c.initial_w)
+    << "\ninit_noise = " << D(c.init_noise) << "\nseed = " << c.seed
+    << "\nprimal_tol = " << D(c.primal_tol) << "\nadjoint_tol = " << D(c.adjoint_tol)
+    << "\nmax_inner = " << c.max_inner << "\nadjoint_stop = " << c.adjoint_stop
+    << "\nadjoint_kernel = " << c.adjoint_kernel << "\nadjoint_cache = " << c.adjoint_cache
+    << "\nmove_limit = " << D(c.move_limit) << "\nthreshold_points = " << c.threshold_points
+    << "\nrecord_interval = " << c.record_interval << "\nworkers = " << c.workers << "\n";
+  o << "\n[output]\ndir = " << c.out_dir << "\nwrite_vtk = " << (c.write_vtk ? "true" : "false")
+    << "\nwrite_csv = " << (c.write_csv ? "true" : "false") << "\n";
+  return o.str();
+}
+
+// parse_zeta_stages (config.cpp:429-452); empty -> one stage {0, zeta}.
+bool zeta_stages(const CaseSpec& c, std::vector<std::pair<long, double>>& st, std::string& err) {
+  try {
+    st.clear();
+    if (c.zeta_stages.empty()) {
+      st.push_back({0, c.zeta});
+      return true;
+    }
+    std::istringstream in(c.zeta_stages);
+    std::string item;
+    while (std::getline(in, item, ',')) {
+      const auto colon = item.find(':');
+      if (colon == std::string::npos)
+        throw CfgError{"zeta_stages entries must look like start:value, got '" + item + "'"};
+      const long start = parse_long(trim(item.substr(0, colon)), "<zeta_stages>", 0, "zeta_stages");
+      const double value =
+          parse_double(trim(item.substr(colon + 1)), "<zeta_stages>", 0, "zeta_stages");
+      if (value < 0) throw CfgError{"zeta stage values must be non-negative"};
+      if (!st.empty() && start <= st.back().first)
+        throw CfgError{"zeta stage starts must increase"};
+      st.push_back({start, value});
+    }
+    if (st.empty() || st.front().first != 0)
+      throw CfgError{"zeta_stages must begin with a stage at iteration 0"};
+    return true;
+  } catch (const CfgError& e) {
+    err = e.msg;
+    return false;
+  }
+}
 
 bool build_system(const CaseSpec& c, SystemArrays& s, std::string& err) {
   try {

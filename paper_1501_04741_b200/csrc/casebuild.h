@@ -55,6 +55,18 @@ struct SystemArrays {
 // + validate. Returns false with a message on error.
 bool parse_case(const std::string& text, const std::string& overrides, CaseSpec& out,
                 std::string& err);
+// CaseConfig::parse_text alone (no overrides, no validation).
+bool parse_case_text(const std::string& text, const std::string& origin, CaseSpec& out,
+                     std::string& err);
+// CaseConfig::set for one dotted key (syntax / unknown-key errors only).
+bool set_case_key(CaseSpec& c, const std::string& dotted, const std::string& value,
+                  std::string& err);
+// CaseConfig::validate.
+bool check_case(const CaseSpec& c, std::string& err);
+// CaseConfig::serialize.
+std::string serialize_case(const CaseSpec& c);
+// parse_zeta_stages: (start, value) pairs.
+bool zeta_stages(const CaseSpec& c, std::vector<std::pair<long, double>>& st, std::string& err);
 // build_tags / build_design / build_objective.
 bool build_system(const CaseSpec& c, SystemArrays& out, std::string& err);
 // The same tables for one x-slab [x0, x0+span) in a local array of nxl

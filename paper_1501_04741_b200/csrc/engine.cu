@@ -756,11 +756,11 @@ struct lbgpu_engine {
   // r <= tol is undone from a snapshot and replayed, so the stop iteration
   // and final state are exactly the per-step loop's.
   void solve(int which, double tol, long long max_iter, long long fixed, int kernel,
-             long long* iters, double* resid, int* conv) {
+             long long* iters, double* resid, int* conv, bool reset_v = true) {
     require_solo();
     const long long n = fixed >= 0 ? fixed : max_iter;
     const char* what = which == 0 ? "iteration" : "adjoint iteration";
-    if (which == 1) {
+    if (which == 1 && reset_v) {
       CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
       CU(cudaMemsetAsync(v[1 - vc], 0, field_bytes(), st));
     }
@@ -1011,21 +1011,24 @@ struct lbgpu_engine {
     release();
   }
 
-  void one_shot(long long iters, const double* zeta, const double* lambda, long long ri,
-                lbgpu_run_row* rows, long long cap, long long* nrows) {
+  // Iterations it0 .. it0+count-1 of a one-shot run of `total` iterations
+  // (zeta/lambda indexed from it0); rows at it % ri == 0 and at it == total.
+  void one_shot(long long it0, long long count, long long total, const double* zeta,
+                const double* lambda, long long ri, lbgpu_run_row* rows, long long cap,
+                long long* nrows) {
     require_solo();
     long long k = 0;
     reset_flags();
     const long long n = (long long)design.size();
-    for (long long it = 1; it <= iters; ++it) {
-      const bool rec = (it % ri == 0) || it == iters;
+    for (long long it = it0; it < it0 + count; ++it) {
+      const bool rec = (it % ri == 0) || it == total;
       if (rec) CU(cudaMemsetAsync(d_flags, 0, sizeof(unsigned long long), st));
       primal_launch(rec, nullptr);
       adjoint_launch(0, false, nullptr);
       if (rec) CU(cudaMemsetAsync(d_flags + 2, 0, sizeof(unsigned long long), st));
       const Launch a = launch(adjoint_steps);
-      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1], 0);
-      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - 1], lambda[it - 1], 0);
+      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0);
+      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0);
       CU(cudaGetLastError());
       if (exact) {  // the device moved w: refresh the host copy and the libm pow tables
         CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
@@ -1044,8 +1047,8 @@ struct lbgpu_engine {
         const double gn = bits_to_double(h_flags[2]);
         row.objective = objective();
         row.penalty = penalty();
-        row.penalty_weight = lambda[it - 1];
-        row.composite = row.objective - lambda[it - 1] * row.penalty;
+        row.penalty_weight = lambda[it - it0];
+        row.composite = row.objective - lambda[it - it0] * row.penalty;
         row.grad_norm = gn;
         if (k < cap && rows) rows[k] = row;
         ++k;
@@ -1563,8 +1566,30 @@ int lbgpu_one_shot(lbgpu_engine* e, int64_t iterations, const double* zeta, cons
   if (!zeta || !lambda || !n_rows || record_interval < 1 || iterations < 0) return LBGPU_E_ARG;
   return guarded(e, [&] {
     long long nr = 0;
-    e->one_shot(iterations, zeta, lambda, record_interval, rows, cap, &nr);
+    e->one_shot(1, iterations, iterations, zeta, lambda, record_interval, rows, cap, &nr);
     *n_rows = nr;
+  });
+}
+
+int lbgpu_one_shot_range(lbgpu_engine* e, int64_t first, int64_t count, int64_t total,
+                         const double* zeta, const double* lambda, int64_t record_interval,
+                         lbgpu_run_row* rows, int64_t cap, int64_t* n_rows) {
+  if (!zeta || !lambda || !n_rows || record_interval < 1 || count < 0 || first < 1)
+    return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long nr = 0;
+    e->one_shot(first, count, total, zeta, lambda, record_interval, rows, cap, &nr);
+    *n_rows = nr;
+  });
+}
+
+int lbgpu_continue_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_t fixed,
+                           int kernel, int64_t* iters, double* residual, int* converged) {
+  if (!iters || !residual || !converged || (kernel != 0 && kernel != 1)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long it = 0;
+    e->solve(1, tol, max_iter, fixed, kernel, &it, residual, converged, false);
+    *iters = it;
   });
 }
 
