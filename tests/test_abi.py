@@ -9,9 +9,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    text = open(os.path.join(ROOT, "include", "lbgpu.h")).read()
-    return sorted(set(re.findall(r"\b(lbgpu_[a-z_0-9]+)\s*\(", text)))
+def declared_symbols(header="lbgpu.h", prefix="lbgpu_"):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(" + prefix + r"[a-z_0-9]+)\s*\(", text)))
 
 
 def test_exports_every_declared_symbol(lbgpu):
@@ -20,6 +20,18 @@ def test_exports_every_declared_symbol(lbgpu):
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
+
+
+def test_exports_the_reference_case_api(lbgpu):
+    """include/lbopt_gpu.h: every function of the reference's lbopt.h
+    (lbopt.h:26-61) is exported by liblbgpu.so."""
+    L = lbgpu.load_library()
+    syms = declared_symbols("lbopt_gpu.h", "lbopt_")
+    assert len(syms) == 27
+    assert not [s for s in syms if not hasattr(L, s)]
+    import ctypes as C
+    L.lbopt_version.restype = C.c_char_p
+    assert L.lbopt_version() == b"0.1.0"
 
 
 def test_version(lbgpu):
