@@ -30,7 +30,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblbgpu.so")
+LIB_PATH = os.environ.get("LBGPU_LIB") or os.path.join(HERE, "liblbgpu.so")
 
 OK, E_ARG, E_CONFIG, E_NUMERIC, E_IO, E_STATE = range(6)
 

@@ -15,11 +15,12 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "liblbgpu.so")
+OBJ = os.environ.get("LBGPU_BUILD_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("LBGPU_LIB") or os.path.join(HERE, "liblbgpu.so")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+EXTRA = os.environ.get("LBGPU_NVCC_EXTRA", "").split()
+COMMON = [*EXTRA, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr", f"-I{os.path.join(os.path.dirname(HERE), 'include')}"]
 
 

@@ -220,15 +220,11 @@ __device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double om
   const R a0 = R(1) - R(1.5) * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
   const R b0 = R(1) - R(1.5) * (up[0] * up[0] + up[1] * up[1] + up[2] * up[2]);
 
-  // r = A^T vf
-  R* r = outf;  // r lives in the output registers until the final update
-  if constexpr (CK == 0) {
-    const R c = R(1.0 - M.om);
-#pragma unroll
-    for (int j = 0; j < L::MF; ++j) r[j] = c * vf[j];
-  } else {
-#pragma unroll
-    for (int j = 0; j < L::MF; ++j) r[j] = R(0);
+  // r = A^T vf = sum_i U_i^T c_i (U_i . vf) over the relaxing rows (A is
+  // symmetric). Only the few row moments mm_i are kept; r_j is rebuilt where
+  // it is used, which keeps ~M fewer values live than storing r.
+  R mm[L::MF];
+  if constexpr (CK != 0) {
     LBGPU_FOR(I, 0, L::MF, {
       if constexpr (L::row_class(I) == 1 || (CK == 2 && L::row_class(I) == 2)) {
         R m = R(0);
@@ -236,21 +232,32 @@ __device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double om
           constexpr double uij = L::U(I, J);
           if constexpr (uij != 0.0) m += R(uij) * vf[J];
         });
-        m *= R(M.mrt_c[I]);
-        LBGPU_FOR(J, 0, L::MF, {
-          constexpr double uij = L::U(I, J);
-          if constexpr (uij != 0.0) r[J] += R(uij) * m;
-        });
+        mm[I] = m * R(M.mrt_c[I]);
       }
     });
   }
+  const R cb = R(1.0 - M.om);
+  auto rj = [&]<int J>() -> R {
+    if constexpr (CK == 0) {
+      return cb * vf[J];
+    } else {
+      R acc = R(0);
+      LBGPU_FOR(I, 0, L::MF, {
+        if constexpr (L::row_class(I) == 1 || (CK == 2 && L::row_class(I) == 2)) {
+          constexpr double uij = L::U(I, J);
+          if constexpr (uij != 0.0) acc += R(uij) * mm[I];
+        }
+      });
+      return acc;
+    }
+  };
 
   R Pr = R(0), Rr = R(0), P0 = R(0), R0 = R(0);
   R Pu[3] = {R(0), R(0), R(0)}, Ru[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MF, {
     const R eu = edotp<L, R, J>(u), eup = edotp<L, R, J>(up);
     const R tv = R(L::wf(J)) * vf[J];
-    const R tr = R(L::wf(J)) * r[J];
+    const R tr = R(L::wf(J)) * rj.template operator()<J>();
     Pr += tv * (b0 + eup * (R(3) + R(4.5) * eup));
     Rr += tr * (a0 + eu * (R(3) + R(4.5) * eu));
     P0 += tv;
@@ -283,7 +290,7 @@ __device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double om
   for (int a = 0; a < 3; ++a) c[a] = G * (Pu[a] + s3 * St1[a]) - Ru[a];
   const R s0 = Pr - Rr - (c[0] * u[0] + c[1] * u[1] + c[2] * u[2]) * inv;
   const R ci[3] = {c[0] * inv, c[1] * inv, c[2] * inv};
-  LBGPU_FOR(K_, 0, L::MF, { outf[K_] = r[K_] + s0 + edotp<L, R, K_>(ci); });
+  LBGPU_FOR(K_, 0, L::MF, { outf[K_] = rj.template operator()<K_>() + s0 + edotp<L, R, K_>(ci); });
   const R om1 = R(1) - om, oms = om * sigma;
 #pragma unroll
   for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k] + oms;
@@ -829,8 +836,12 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
   }
   }
 
+#ifndef LBGPU_ADJ_MINB
+#define LBGPU_ADJ_MINB 4
+#endif
+
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint(Launch a,
+__global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint(Launch a,
                                                                 const R* __restrict__ base,
                                                                 const R* __restrict__ src,
                                                                 R* __restrict__ dst) {
@@ -842,7 +853,7 @@ __global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint(Launch a,
 }
 
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void __launch_bounds__(128, SPLIT ? 4 : 1) k_adjoint_cols(Launch a,
+__global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint_cols(Launch a,
                                                                      const R* __restrict__ base,
                                                                      const R* __restrict__ src,
                                                                      R* __restrict__ dst, int c0,
