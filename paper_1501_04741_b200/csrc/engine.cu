@@ -33,9 +33,11 @@ struct Fail {
 #define CU(call)                                                                         \
   do {                                                                                   \
     const cudaError_t e_ = (call);                                                       \
-    if (e_ != cudaSuccess)                                                               \
+    if (e_ != cudaSuccess) {                                                             \
+      (void)cudaGetLastError(); /* a failed call must not poison the next check */       \
       throw Fail{LBGPU_E_NUMERIC, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
                                       " (" #call ")"};                                   \
+    }                                                                                    \
   } while (0)
 
 // NCCL is resolved at run time: a process that already loaded libnccl
@@ -595,7 +597,8 @@ struct lbgpu_engine {
   void raise_bad(unsigned long long key, const char* what) {
     const long long gidx = (long long)(key & kIdxMask);
     const long long step = (long long)(key >> 40);
-    const int x = int(gidx % nx), y = int((gidx / nx) % ny), z = int(gidx / ((long long)nx * ny));
+    // keys hold the GLOBAL flat index (gflat): decode with the global x extent
+    const int x = int(gidx % gnx), y = int((gidx / gnx) % ny), z = int(gidx / ((long long)gnx * ny));
     reset_flags();
     throw Fail{LBGPU_E_NUMERIC, "non-positive density at node (" + std::to_string(x) + "," +
                                     std::to_string(y) + "," + std::to_string(z) + ") (" + what +
@@ -729,6 +732,9 @@ struct lbgpu_engine {
   void init_state() {
     if (exact) exact::init_state(N, dim, prec, f[fc], st);
     else fast::init_state(N, dim, prec, f[fc], st);
+    // ghost layout: sweeps write owned columns only, so both ping-pong buffers
+    // carry the same ghost columns until an exchange refreshes them
+    if (ghosts) CU(cudaMemcpyAsync(f[1 - fc], f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
     CU(cudaGetLastError());
   }
@@ -967,6 +973,9 @@ struct lbgpu_engine {
       for (long long i = 0; i < nslots + 3; ++i) {
         void* p = nullptr;
         CU(cudaMalloc(&p, field_bytes()));
+        // ghost layout: sweeps write owned columns only, so seed every slot's
+        // ghosts with the current ones (the exchange refreshes them in NCCL mode)
+        if (ghosts) CU(cudaMemcpyAsync(p, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
         slots.push_back(p);
       }
       void* s0 = slots[0];     // state 0 (checkpoint)

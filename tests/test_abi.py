@@ -60,3 +60,22 @@ def test_null_handle_is_arg_error(lbgpu):
     assert L.lbgpu_error_message(None) == b"null handle"
     r = C.c_double()
     assert L.lbgpu_primal_step(None, 1, C.byref(r)) == lbgpu.E_ARG
+
+
+def test_headers_compile_as_c_and_link(lbgpu, tmp_path):
+    """include/lbgpu.h and include/lbopt_gpu.h are plain C: a C99 consumer
+    compiles with -Wall -Werror, links against liblbgpu.so and runs its
+    host-only calls."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("no gcc")
+    lib = os.path.dirname(lbgpu.LIB_PATH)
+    exe = str(tmp_path / "consumer")
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "consumer.c"), "-o", exe, "-L", lib,
+                    "-llbgpu", "-Wl,-rpath," + lib], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    assert out.stdout.startswith("ok 0.1.0")
