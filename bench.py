@@ -164,7 +164,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -244,18 +244,18 @@ def main() -> None:
 
     # e2e through the public C ABI with host buffers: each step uploads the
     # design vector (DesignField::nodes order, as a host-side optimizer such as
-    # the reference's MMA update produces it) from pinned host memory
-    # (lbgpu_set_design_values) and runs one primal and one adjoint sweep,
-    # each returning its step residual to the host (lbgpu_primal_step /
-    # lbgpu_adjoint_step).
+    # the reference's MMA update produces it, optimizer.cpp:200-202) from
+    # pinned host memory and runs one primal sweep — one call,
+    # lbgpu_primal_step_with_design, which pipelines the upload under the
+    # sweep — then one adjoint sweep (lbgpu_adjoint_step); each call returns
+    # its step residual to the host.
     w_host = torch.from_numpy(eng.design_values()).pin_memory()
     w_np = w_host.numpy()
     eng.set_design_values(w_np)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        eng.set_design_values(w_np)
-        eng.primal_step(1)
+        eng.primal_step_with_design(w_np, 1)
         eng.adjoint_step(1)
     torch.cuda.synchronize(local)
     e2e_s = time.perf_counter() - t0
@@ -266,8 +266,8 @@ def main() -> None:
     e2e = {"value": world * nodes * args.e2e_steps / e2e_s / 1e6, "unit": "MLUPS",
            "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": 16,
            "steps": args.e2e_steps,
-           "path": "lbgpu_set_design_values(pinned host w) + lbgpu_primal_step + "
-                   "lbgpu_adjoint_step (each returns its residual)"}
+           "path": "lbgpu_primal_step_with_design(pinned host w) + lbgpu_adjoint_step "
+                   "(each returns its residual)"}
 
     if rank != 0:
         if dist:

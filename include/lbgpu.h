@@ -145,6 +145,13 @@ int lbgpu_get_design_values(lbgpu_engine* e, double* w_design);
 /* n x primal_step (collision.cpp:308-363); residual (nullable) = step_residual
  * of the last step (collision.cpp:365-375). */
 int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual);
+/* optimizer.cpp:200-202: write new design values (DesignField::nodes order,
+ * host memory; pinned overlaps best) into w, then n >= 1 primal steps. The
+ * upload is pipelined under the first sweep in z-chunks. Equivalent to
+ * lbgpu_set_design_values + lbgpu_primal_step; the buffer is consumed when the
+ * call returns. residual (nullable) as lbgpu_primal_step. */
+int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64_t n,
+                                  double* residual);
 /* n x adjoint_step (adjoint.cpp:206-254) against the current primal state.
  * kernel: 0 analytic, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18). */
 int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual);

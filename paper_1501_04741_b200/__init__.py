@@ -103,6 +103,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_set_design_values.argtypes = [vp, vp]
     L.lbgpu_get_design_values.argtypes = [vp, vp]
     L.lbgpu_primal_step.argtypes = [vp, i64, dp]
+    L.lbgpu_primal_step_with_design.argtypes = [vp, vp, i64, dp]
     L.lbgpu_adjoint_step.argtypes = [vp, i64, C.c_int, dp]
     L.lbgpu_solve_primal.argtypes = [vp, C.c_double, i64, i64, C.POINTER(i64), dp,
                                      C.POINTER(C.c_int)]
@@ -288,6 +289,17 @@ class Engine:
         w_design = np.ascontiguousarray(w_design, np.float64)
         assert w_design.size == self.n_design
         self._ok(self.L.lbgpu_set_design_values(self.h, _ptr(w_design)))
+
+    def primal_step_with_design(self, w_design: np.ndarray, n: int = 1,
+                                residual: bool = True) -> float | None:
+        """New design values (DesignField::nodes order) then n primal steps,
+        the upload pipelined under the first sweep (optimizer.cpp:200-202)."""
+        w_design = np.ascontiguousarray(w_design, np.float64)
+        assert w_design.size == self.n_design
+        r = C.c_double()
+        self._ok(self.L.lbgpu_primal_step_with_design(self.h, _ptr(w_design), n,
+                                                      C.byref(r) if residual else None))
+        return r.value if residual else None
 
     def design_values(self) -> np.ndarray:
         out = np.empty(max(self.n_design, 1))

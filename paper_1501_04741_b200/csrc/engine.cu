@@ -153,21 +153,31 @@ void model_rows(std::vector<double>& U, std::vector<int>& cls) {
 
 // ------------------------------------------------------- pairwise tree
 // pairwise_sum_fn (reduce.hpp:43-52): leaves of <= 16 terms from midpoint
-// splits, combined in the recursion's post-order. The shape depends only on
-// n, so it is built once on the host and replayed on the device.
+// splits, each combine adding its two halves. The shape depends only on n, so
+// it is built once on the host and replayed on the device. Every combine is
+// one fixed addition of two fixed operands, so any schedule that runs a
+// combine after its children gives the reference's bits: the ops are grouped
+// by height (all children one level down or more) and each level runs in
+// parallel — wide levels as their own launch, the narrow top of the tree in
+// one block with a barrier per level.
 struct PairTree {
+  static constexpr int kTopOps = 2048;  // levels narrower than this: single-block kernel
   long long n = -1;
   int leaves = 0, ops = 0;
   long long* d_lo = nullptr;
   long long* d_hi = nullptr;
-  int2* d_ops = nullptr;
+  int2* d_ops = nullptr;   // sorted by height; op k writes vals[leaves + k]
+  int* d_lvl = nullptr;    // level offsets into d_ops (top levels)
   double* d_vals = nullptr;
+  std::vector<int> lvl;    // level offsets, lvl.size() = levels + 1
+  int top = 0;             // first level handled by the single-block kernel
 
   void build(long long count) {
     release();
     n = count;
     std::vector<long long> lo, hi;
     std::vector<std::pair<int, int>> tmp;  // encoded child ids
+    std::vector<int> height;
     std::function<int(long long, long long)> rec = [&](long long a, long long b) -> int {
       if (b - a <= 16) {
         lo.push_back(a);
@@ -176,15 +186,26 @@ struct PairTree {
       }
       const long long mid = a + (b - a) / 2;
       const int x = rec(a, mid), y = rec(mid, b);
+      auto h = [&](int id) { return id >= 0 ? 0 : height[-id - 1]; };
       tmp.push_back({x, y});
+      height.push_back(1 + std::max(h(x), h(y)));
       return -int(tmp.size());  // internal id -k (k = 1-based post-order)
     };
     rec(0, count);
     leaves = int(lo.size());
     ops = int(tmp.size());
-    auto dec = [&](int id) { return id >= 0 ? id : leaves + (-id - 1); };
+    const int levels = ops ? *std::max_element(height.begin(), height.end()) : 0;
+    lvl.assign(levels + 1, 0);
+    for (int k = 0; k < ops; ++k) ++lvl[height[k]];  // counts at index h (1-based)
+    for (int h = 1; h <= levels; ++h) lvl[h] += lvl[h - 1];  // lvl[h] = end of level h
+    // lvl[h-1] .. lvl[h] is level h; stable placement keeps post-order within a level
+    std::vector<int> pos(ops), fill(lvl.begin(), lvl.end());
+    for (int k = 0; k < ops; ++k) pos[k] = fill[height[k] - 1]++;
+    auto dec = [&](int id) { return id >= 0 ? id : leaves + pos[-id - 1]; };
     std::vector<int2> o(ops);
-    for (int k = 0; k < ops; ++k) o[k] = make_int2(dec(tmp[k].first), dec(tmp[k].second));
+    for (int k = 0; k < ops; ++k) o[pos[k]] = make_int2(dec(tmp[k].first), dec(tmp[k].second));
+    top = levels;
+    while (top > 0 && lvl[top] - lvl[top - 1] < kTopOps) --top;  // levels top+1.. are narrow
     CU(cudaMalloc(&d_lo, sizeof(long long) * leaves));
     CU(cudaMalloc(&d_hi, sizeof(long long) * leaves));
     CU(cudaMalloc(&d_vals, sizeof(double) * (leaves + ops + 1)));
@@ -193,11 +214,14 @@ struct PairTree {
     if (ops) {
       CU(cudaMalloc(&d_ops, sizeof(int2) * ops));
       CU(cudaMemcpy(d_ops, o.data(), sizeof(int2) * ops, cudaMemcpyHostToDevice));
+      CU(cudaMalloc(&d_lvl, sizeof(int) * lvl.size()));
+      CU(cudaMemcpy(d_lvl, lvl.data(), sizeof(int) * lvl.size(), cudaMemcpyHostToDevice));
     }
   }
   void release() {
-    cudaFree(d_lo), cudaFree(d_hi), cudaFree(d_ops), cudaFree(d_vals);
-    d_lo = d_hi = nullptr, d_ops = nullptr, d_vals = nullptr, n = -1;
+    cudaFree(d_lo), cudaFree(d_hi), cudaFree(d_ops), cudaFree(d_vals), cudaFree(d_lvl);
+    d_lo = d_hi = nullptr, d_ops = nullptr, d_vals = nullptr, d_lvl = nullptr, n = -1;
+    lvl.clear();
   }
 };
 
@@ -210,10 +234,23 @@ __global__ void k_leaf_sums(const double* __restrict__ t, const long long* lo, c
   vals[i] = s;
 }
 
-// Post-order combine; a single thread keeps the reference's exact order.
-__global__ void k_combine(double* vals, const int2* ops, int leaves, int nops, double* out) {
-  for (int k = 0; k < nops; ++k) vals[leaves + k] = vals[ops[k].x] + vals[ops[k].y];
-  *out = nops ? vals[leaves + nops - 1] : vals[0];
+// One wide level of combines [b, e).
+__global__ void k_combine_level(double* vals, const int2* __restrict__ ops, int leaves, int b, int e) {
+  const int k = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < e) vals[leaves + k] = vals[ops[k].x] + vals[ops[k].y];
+}
+
+// The narrow levels first+1 .. levels in one block, a barrier between levels;
+// writes the root (or the single leaf) to *out.
+__global__ void __launch_bounds__(1024) k_combine_top(double* vals, const int2* __restrict__ ops,
+                                                      const int* __restrict__ lvl, int leaves,
+                                                      int first, int levels, int nops, double* out) {
+  for (int h = first + 1; h <= levels; ++h) {
+    for (int k = lvl[h - 1] + threadIdx.x; k < lvl[h]; k += blockDim.x)
+      vals[leaves + k] = vals[ops[k].x] + vals[ops[k].y];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = nops ? vals[leaves + nops - 1] : vals[0];
 }
 
 __global__ void k_scatter_design(const double* __restrict__ vals, const long long* __restrict__ nodes,
@@ -252,6 +289,8 @@ struct lbgpu_engine {
   void* halo_buf[4] = {nullptr, nullptr, nullptr, nullptr};  // send L, send R, recv L, recv R
   cudaStream_t st_comm = nullptr;  // halo traffic overlaps the interior columns
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+  cudaStream_t st_h2d = nullptr;        // design uploads pipelined under the first sweep
+  std::vector<cudaEvent_t> ev_chunk;    // one per z-chunk of that upload (+1: start)
   bool owns_stream = true;
   long long N = 0;
   int device = 0;
@@ -262,7 +301,7 @@ struct lbgpu_engine {
   std::vector<uint8_t> tag, mask, code;
   std::vector<double> w, bc_T, A, relax;
   std::vector<int8_t> bc_axis, bc_sign;
-  std::vector<long long> design, support, inlets, adj_side;
+  std::vector<long long> design, support, inlets, adj_side, grad_side;
   // device
   void* f[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -273,6 +312,7 @@ struct lbgpu_engine {
   double *d_A = nullptr, *d_At = nullptr;
   long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr;
   long long* d_adj_side = nullptr;
+  long long* d_grad_side = nullptr;
   double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
   double* d_ref = nullptr;
   double* d_wvals = nullptr;  // staging for design-order uploads
@@ -297,12 +337,14 @@ struct lbgpu_engine {
     if (ev_bnd) cudaEventDestroy(ev_bnd);
     if (ev_halo) cudaEventDestroy(ev_halo);
     if (st_comm) cudaStreamDestroy(st_comm);
+    for (cudaEvent_t ev : ev_chunk) cudaEventDestroy(ev);
+    if (st_h2d) cudaStreamDestroy(st_h2d);
     for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
-    cudaFree(d_adj_side), cudaFree(d_wvals);
+    cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -421,6 +463,10 @@ struct lbgpu_engine {
     for (long long i : support)
       if (M.obj_kind == 2 || tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) adj_side.push_back(i);
     up_list(adj_side, d_adj_side);
+    // design positions on non-Interior nodes: the gradient's dual side launch
+    for (size_t i = 0; i < design.size(); ++i)
+      if (tag[design[i]] != TAG_INTERIOR) grad_side.push_back((long long)i);
+    up_list(grad_side, d_grad_side);
     const size_t nt = std::max({design.size(), support.size(), inlets.size(), size_t(1)});
     CU(cudaMalloc(&d_terms, sizeof(double) * nt));
     CU(cudaMalloc(&d_grad, sizeof(double) * std::max<size_t>(design.size(), 1)));
@@ -438,6 +484,7 @@ struct lbgpu_engine {
       refresh_pow_tables();
     }
     T.code = d_code, T.w = d_w, T.bcT = d_bcT, T.p0 = d_p0, T.p1 = d_p1;
+    T.grad_side = d_grad_side, T.n_grad_side = (long long)grad_side.size();
     G = Geom{nx, ny, nz, 0, span, N, x0, gnx, ny};
     init_state();
     CU(cudaStreamSynchronize(st));
@@ -756,6 +803,89 @@ struct lbgpu_engine {
     return want_resid ? bits_to_double(h_flags[0]) : 0.0;
   }
 
+  // New design values (DesignField::nodes order, host memory) followed by n
+  // primal sweeps: optimizer.cpp:200-202 (the MMA update's write-back, then
+  // solve_fixed_point). The first sweep runs in z-chunks, each waiting only
+  // for its own slice of the upload, so the H2D copy overlaps the sweep
+  // (design nodes ascend in flat index, i.e. z-major, and a sweep node
+  // reads w only at itself). Falls back to upload-then-sweep where chunking
+  // does not apply (exact build: host pow tables; 2D; NCCL halo overlap).
+  static constexpr int kChunks = 8;
+  double design_steps(const double* wd, long long nsteps, bool want_resid) {
+    require_solo();
+    const long long n = (long long)design.size();
+    if (!n || exact || dim == 2 || xmode == 2 || nz < 2 * kChunks) {
+      upload_design_values(wd);
+      return steps(0, nsteps, 0, want_resid);
+    }
+    if (nsteps <= 0) return 0.0;
+    if (!d_wvals) CU(cudaMalloc(&d_wvals, sizeof(double) * n));
+    if (!st_h2d) {
+      CU(cudaStreamCreateWithFlags(&st_h2d, cudaStreamNonBlocking));
+      ev_chunk.resize(kChunks + 1);
+      for (cudaEvent_t& ev : ev_chunk) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    reset_flags();
+    // the staging buffer is free once everything queued before us has run
+    CU(cudaEventRecord(ev_chunk[kChunks], st));
+    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
+    const long long plane = (long long)nx * ny;
+    long long ib[kChunks + 1];
+    int zb[kChunks + 1];
+    for (int c = 0; c <= kChunks; ++c) {
+      zb[c] = int((long long)nz * c / kChunks);
+      ib[c] = std::lower_bound(design.begin(), design.end(), plane * zb[c]) - design.begin();
+    }
+    for (int c = 0; c < kChunks; ++c)
+      if (ib[c + 1] > ib[c]) {
+        CU(cudaMemcpyAsync(d_wvals + ib[c], wd + ib[c], sizeof(double) * (ib[c + 1] - ib[c]),
+                           cudaMemcpyHostToDevice, st_h2d));
+        CU(cudaEventRecord(ev_chunk[c], st_h2d));
+      }
+    ++primal_steps;
+    ++launches;
+    const bool r0 = want_resid && nsteps == 1;
+    for (int c = 0; c < kChunks; ++c) {
+      const long long m_ = ib[c + 1] - ib[c];
+      if (m_ > 0) {
+        CU(cudaStreamWaitEvent(st, ev_chunk[c], 0));
+        k_scatter_design<<<unsigned((m_ + 255) / 256), 256, 0, st>>>(d_wvals + ib[c], d_design + ib[c],
+                                                                     m_, d_w);
+      }
+      SweepArgs sa = sweep(primal_steps, r0, nullptr);
+      sa.z0 = zb[c], sa.z1 = zb[c + 1];
+      if (exact) exact::primal(sa, f[fc], f[1 - fc]);
+      else fast::primal(sa, f[fc], f[1 - fc]);
+    }
+    launches += 2 * kChunks - 1;
+    fc ^= 1;
+    w_host_stale = true;
+    for (long long k = 1; k < nsteps; ++k) primal_launch(want_resid && k == nsteps - 1, nullptr);
+    CU(cudaGetLastError());
+    reduce_flags(d_flags, 1, false);
+    reduce_flags(d_flags + 1, 1, true);
+    pull_flags();  // also: the host buffer has been consumed when we return
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+    return want_resid ? bits_to_double(h_flags[0]) : 0.0;
+  }
+  // lbgpu_set_design_values: design-order values -> device w (synchronous)
+  void upload_design_values(const double* w_design) {
+    const long long n = (long long)design.size();
+    if (!n) return;
+    if (!d_wvals) CU(cudaMalloc(&d_wvals, sizeof(double) * n));
+    CU(cudaMemcpyAsync(d_wvals, w_design, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    k_scatter_design<<<unsigned((n + 255) / 256), 256, 0, st>>>(d_wvals, d_design, n, d_w);
+    ++launches;
+    CU(cudaGetLastError());
+    if (exact) {  // the libm pow tables follow the host copy
+      for (long long i = 0; i < n; ++i) w[design[i]] = w_design[i];
+      refresh_pow_tables();
+    } else {
+      w_host_stale = true;
+      sync();
+    }
+  }
+
   // solve_fixed_point / solve_adjoint stop rule (collision.cpp:377-416,
   // adjoint.cpp:256-297), batched: every step writes its residual into a ring
   // slot, the host scans once per batch, and an overshoot past the first
@@ -840,7 +970,13 @@ struct lbgpu_engine {
   double pairwise(PairTree& tr, const double* d_t) {
     const int nb = (tr.leaves + 127) / 128;
     k_leaf_sums<<<nb, 128, 0, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_vals);
-    k_combine<<<1, 1, 0, st>>>(tr.d_vals, tr.d_ops, tr.leaves, tr.ops, d_scalar);
+    for (int h = 1; h <= tr.top; ++h) {
+      const int b = tr.lvl[h - 1], e = tr.lvl[h];
+      k_combine_level<<<unsigned((e - b + 255) / 256), 256, 0, st>>>(tr.d_vals, tr.d_ops, tr.leaves, b, e);
+    }
+    k_combine_top<<<1, 1024, 0, st>>>(tr.d_vals, tr.d_ops, tr.d_lvl, tr.leaves, tr.top,
+                                      int(tr.lvl.size()) - 1, tr.ops, d_scalar);
+    launches += 2 + tr.top;
     double out = 0.0;
     CU(cudaMemcpyAsync(&out, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
     sync();
@@ -1490,21 +1626,7 @@ int lbgpu_get_design(const lbgpu_engine* e, double* w_full) {
 
 int lbgpu_set_design_values(lbgpu_engine* e, const double* w_design) {
   if (!w_design) return LBGPU_E_ARG;
-  return guarded(e, [&] {
-    const long long n = (long long)e->design.size();
-    if (!n) return;
-    if (!e->d_wvals) CU(cudaMalloc(&e->d_wvals, sizeof(double) * n));
-    CU(cudaMemcpyAsync(e->d_wvals, w_design, sizeof(double) * n, cudaMemcpyHostToDevice, e->st));
-    k_scatter_design<<<unsigned((n + 255) / 256), 256, 0, e->st>>>(e->d_wvals, e->d_design, n, e->d_w);
-    CU(cudaGetLastError());
-    if (e->exact) {  // the libm pow tables follow the host copy
-      for (long long i = 0; i < n; ++i) e->w[e->design[i]] = w_design[i];
-      e->refresh_pow_tables();
-    } else {
-      e->w_host_stale = true;
-      e->sync();
-    }
-  });
+  return guarded(e, [&] { e->upload_design_values(w_design); });
 }
 
 int lbgpu_get_design_values(lbgpu_engine* e, double* w_design) {
@@ -1523,6 +1645,15 @@ int lbgpu_get_design_values(lbgpu_engine* e, double* w_design) {
 int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual) {
   return guarded(e, [&] {
     const double r = e->steps(0, n, 0, residual != nullptr);
+    if (residual) *residual = r;
+  });
+}
+
+int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64_t n,
+                                  double* residual) {
+  if (!w_design || n < 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    const double r = e->design_steps(w_design, n, residual != nullptr);
     if (residual) *residual = r;
   });
 }

@@ -741,7 +741,8 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
                                                 R* __restrict__ dst) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
-  if (x < a.g.x1) primal_body<L, R, CK, RESID>(a, src, dst, x, blockIdx.y, blockIdx.z, rmax);
+  if (x < a.g.x1)
+    primal_body<L, R, CK, RESID>(a, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
@@ -848,7 +849,8 @@ __global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint(Lau
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (x < a.g.x1)
-    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, x, blockIdx.y, blockIdx.z, rmax);
+    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z,
+                                             rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
@@ -898,8 +900,12 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
 // Per-design-node gradient (param_gradient's design part, adjoint.cpp:377-398)
 // with, when UPDATE, the one-shot composite/ascent step fused in
 // (optimizer.cpp:41-45, descent_update :8-16). The node list holds local
-// indices in ascending global order.
-template <class L, class R, int AK, bool UPDATE>
+// indices in ascending global order. The analytic kernel (AK = 0) handles
+// Interior design nodes only — the reference's own split (adjoint.cpp:388-396)
+// — so it carries no dual-number code; design nodes on any other tag (none
+// for config-built cases, config.cpp:355) are the SIDE launch over
+// NodeTables::grad_side with the dual path (design_gradient_node_dual).
+template <class L, class R, int AK, bool UPDATE, bool SIDE>
 __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict__ p,
                                                   const R* __restrict__ q,
                                                   const long long* __restrict__ nodes,
@@ -907,46 +913,51 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
                                                   double* __restrict__ w_rw, double zeta,
                                                   double lambda, int accumulate) {
   using namespace detail;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long cmax = 0;
-  if (i < n) {
+  const long long cnt = SIDE ? a.t.n_grad_side : n;
+  if (t < cnt) {
+    const long long i = SIDE ? a.t.grad_side[t] : t;
     const Geom& g = a.g;
     const long long idx = nodes[i];
-    const int x = int(idx % g.nx);
-    const int y = int((idx / g.nx) % g.ny);
-    const int z = int(idx / ((long long)g.nx * g.ny));
-    const Nbr nb = make_nbr(g, x, y, z);
-    R f[L::M], v[L::M];
-    gather<L, R, -1>(p, g.N, nb, f);
-    gather<L, R, +1>(q, g.N, nb, v);
     const uint8_t code = a.t.code[idx];
-    const double w = a.t.w[idx];
-    const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
-    double gv = 0.0;
-    bool ok;
-    if (AK == 0 && (code & TAG_MASK) == TAG_INTERIOR) {
-      ok = design_gradient<L, R>(a.M, pp, f, f + L::MF, R(w), v, v + L::MF, gv);
-    } else {  // design_gradient_node_dual (adjoint.cpp:361-373)
-      Dual<R> din[L::M], dout[L::M];
+    constexpr bool kAnalytic = AK == 0 && !SIDE;
+    if (!kAnalytic || (code & TAG_MASK) == TAG_INTERIOR) {
+      const int x = int(idx % g.nx);
+      const int y = int((idx / g.nx) % g.ny);
+      const int z = int(idx / ((long long)g.nx * g.ny));
+      const Nbr nb = make_nbr(g, x, y, z);
+      R f[L::M], v[L::M];
+      gather<L, R, -1>(p, g.N, nb, f);
+      gather<L, R, +1>(q, g.N, nb, v);
+      const double w = a.t.w[idx];
+      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
+      double gv = 0.0;
+      bool ok;
+      if constexpr (kAnalytic) {
+        ok = design_gradient<L, R>(a.M, pp, f, f + L::MF, R(w), v, v + L::MF, gv);
+      } else {  // design_gradient_node_dual (adjoint.cpp:361-373)
+        Dual<R> din[L::M], dout[L::M];
 #pragma unroll
-      for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(f[k]);
-      ok = collide_node<L>(a.M, pp, code & TAG_MASK, code_axis(code), code_sign(code),
-                           a.t.bcT[idx], din, Dual<R>(R(w), R(1)), Dual<R>(R(a.M.rho_in)), dout);
-      R acc = R(0);
+        for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(f[k]);
+        ok = collide_node<L>(a.M, pp, code & TAG_MASK, code_axis(code), code_sign(code),
+                             a.t.bcT[idx], din, Dual<R>(R(w), R(1)), Dual<R>(R(a.M.rho_in)), dout);
+        R acc = R(0);
 #pragma unroll
-      for (int k = 0; k < L::M; ++k) acc = acc + v[k] * dout[k].d;
-      gv = double(acc);
-    }
-    if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    if constexpr (UPDATE) {
-      double comp = gv;
-      if (lambda != 0.0) comp -= lambda * (1.0 - 2.0 * w);
-      double wn = w + zeta * comp;
-      wn = wn < 0.0 ? 0.0 : (1.0 < wn ? 1.0 : wn);
-      w_rw[idx] = wn;
-      cmax = (unsigned long long)__double_as_longlong(fabs(comp));
-    } else {
-      gout[i] = accumulate ? gout[i] + gv : gv;
+        for (int k = 0; k < L::M; ++k) acc = acc + v[k] * dout[k].d;
+        gv = double(acc);
+      }
+      if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+      if constexpr (UPDATE) {
+        double comp = gv;
+        if (lambda != 0.0) comp -= lambda * (1.0 - 2.0 * w);
+        double wn = w + zeta * comp;
+        wn = wn < 0.0 ? 0.0 : (1.0 < wn ? 1.0 : wn);
+        w_rw[idx] = wn;
+        cmax = (unsigned long long)__double_as_longlong(fabs(comp));
+      } else {
+        gout[i] = accumulate ? gout[i] + gv : gv;
+      }
     }
   }
   if constexpr (UPDATE) block_max_bits(cmax, a.fl.aux);
@@ -1132,7 +1143,9 @@ void primal_t(const SweepArgs& s, const void* src, void* dst) {
   if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
   if (a.g.x1 <= a.g.x0) return;
   const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-  dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+  int nzs = a.g.nz;
+  if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (pipelined design upload)
+  dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, nzs);
   k_primal<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, in, out);
 }
 template <class L, class R, int CK, int AK, bool RES>
@@ -1222,10 +1235,18 @@ void gradient(const Launch& a, int dim, int prec, int ak, bool update, const voi
   LBGPU_LR_DISPATCH(dim, prec, {
     const R* pp = static_cast<const R*>(p);
     const R* qq = static_cast<const R*>(q);
-    if (ak == 0 && !update) k_gradient<L, R, 0, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
-    else if (ak == 0) k_gradient<L, R, 0, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
-    else if (!update) k_gradient<L, R, 1, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
-    else k_gradient<L, R, 1, true><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    const unsigned ns = unsigned((a.t.n_grad_side + bs - 1) / bs);
+    if (ak == 0 && !update) {
+      k_gradient<L, R, 0, false, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+      if (ns) k_gradient<L, R, 1, false, true><<<ns, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    } else if (ak == 0) {
+      k_gradient<L, R, 0, true, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+      if (ns) k_gradient<L, R, 1, true, true><<<ns, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    } else if (!update) {
+      k_gradient<L, R, 1, false, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    } else {
+      k_gradient<L, R, 1, true, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+    }
   });
 }
 void objective_terms(const Launch& a, int dim, int prec, const void* p, const long long* nodes,

@@ -12,6 +12,7 @@ struct Geom {
   long long N;      // nodes of the local array = plane stride
   int gx_off;       // global x = local x + gx_off
   int gnx, gny;     // global extents (flat index for error reports)
+  int z0 = 0;       // first z plane of a z-chunked sweep (grid.z counts from here)
 };
 
 struct NodeTables {
@@ -20,6 +21,8 @@ struct NodeTables {
   const double* bcT;
   const double* p0;  // exact build: host-glibc pow(base, theta) per node
   const double* p1;  //              pow(base, theta - 1)
+  const long long* grad_side;  // design positions whose node is not Interior (dual gradient)
+  long long n_grad_side;
   PowPair pp_one;    // pow pair of non-design nodes (w == 1)
   double omt_one;    // thermal relaxation rate at w == 1
 };
@@ -46,6 +49,7 @@ struct SweepArgs {
   const long long* adj_side;  // adjoint side-list nodes (k_adjoint_side)
   long long n_adj_side;
   int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
+  int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).

@@ -44,6 +44,6 @@ CASES = {
 }
 
 
-def case_text(name: str) -> str:
+def case_text(name: str, extra: dict | None = None) -> str:
     preset, ov = CASES[name]
-    return preset_text(preset, ov)
+    return preset_text(preset, {**ov, **(extra or {})})

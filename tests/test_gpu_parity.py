@@ -268,3 +268,29 @@ def test_design_values_round_trip(lbgpu, oracle_mod, has_gpu):
         a.primal_step(5)
         b.primal_step(5)
         assert np.array_equal(a.get_state(0), b.get_state(0))
+
+
+@pytest.mark.parametrize("nz", [8, 37])
+def test_primal_step_with_design_equals_upload_then_step(lbgpu, has_gpu, nz):
+    """lbgpu_primal_step_with_design (upload pipelined under the first sweep in
+    z-chunks; nz = 37 gives uneven chunks, nz = 8 takes the fallback) is
+    bitwise set_design_values + primal_step: states, residual, w."""
+    txt = case_text("mix3d", {"lattice.nz": nz})
+    for exact in (False, True):
+        a = lbgpu.Engine.from_config(txt, exact=exact)
+        b = lbgpu.Engine.from_config(txt, exact=exact)
+        for e in (a, b):
+            e.init_state()
+            e.primal_step(20)
+        rng = np.random.default_rng(nz)
+        for k in (1, 3):
+            vals = rng.uniform(0, 1, a.n_design)
+            ra = a.primal_step_with_design(vals, k)
+            b.set_design_values(vals)
+            rb = b.primal_step(k)
+            assert ra == rb
+            assert np.array_equal(a.get_state(0), b.get_state(0))
+            assert np.array_equal(a.design_values(), vals)
+        a.adjoint_step(2)
+        b.adjoint_step(2)
+        assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
