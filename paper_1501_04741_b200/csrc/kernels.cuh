@@ -736,6 +736,9 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* __restrict
   store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
 }
 
+// Plain bounds: ptxas picks 64 regs (FP32) / 96-122 (FP64), no spills. Forcing
+// more blocks spills (FP32 C3 primal GB/s: 64 regs 5748, 48 regs 5480, 40
+// regs 4036); (128, 1) lets it take 106 regs (4827).
 template <class L, class R, int CK, bool RESID>
 __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
                                                 R* __restrict__ dst) {
@@ -837,12 +840,21 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
   }
   }
 
+// Resident blocks per SM the split adjoint is compiled for (register cap
+// 65536 / (128 * minb)). Measured on B200, C3 adjoint GB/s: FP64 minb 4 best
+// (3 and 2 lower); FP32 4: 4197, 5: 4702, 6: 4950, 8: 5215 (64 regs, 24 B
+// stack — the occupancy is worth the spill).
 #ifndef LBGPU_ADJ_MINB
 #define LBGPU_ADJ_MINB 4
 #endif
+#ifndef LBGPU_ADJ_MINB32
+#define LBGPU_ADJ_MINB32 8
+#endif
+#define LBGPU_ADJ_BOUNDS(SPLIT, R) \
+  __launch_bounds__(128, (SPLIT) ? (sizeof(R) == 4 ? LBGPU_ADJ_MINB32 : LBGPU_ADJ_MINB) : 1)
 
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint(Launch a,
+__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R) k_adjoint(Launch a,
                                                                 const R* __restrict__ base,
                                                                 const R* __restrict__ src,
                                                                 R* __restrict__ dst) {
@@ -855,7 +867,7 @@ __global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint(Lau
 }
 
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void __launch_bounds__(128, SPLIT ? LBGPU_ADJ_MINB : 1) k_adjoint_cols(Launch a,
+__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R) k_adjoint_cols(Launch a,
                                                                      const R* __restrict__ base,
                                                                      const R* __restrict__ src,
                                                                      R* __restrict__ dst, int c0,

@@ -39,12 +39,16 @@ def want(c):
 
 
 def sweeps(e, K=50):
+    """Sweep rates over the nodes a sweep updates (a slab's owned columns, not
+    its ghost/pad columns)."""
     e.time_pairs(5)
     t, tp, ta = e.time_pairs(K)
     s = 8 if e.precision == 64 else 4
-    return {"primal_mlups": e.n * K / tp / 1e3, "adjoint_mlups": e.n * K / ta / 1e3,
-            "primal_gbs": 2 * e.m * s * e.n * K / tp / 1e6,
-            "adjoint_gbs": 3 * e.m * s * e.n * K / ta / 1e6}
+    sl = e.slab()
+    n = e.n // sl["nxl"] * sl["span"]
+    return {"primal_mlups": n * K / tp / 1e3, "adjoint_mlups": n * K / ta / 1e3,
+            "primal_gbs": 2 * e.m * s * n * K / tp / 1e6,
+            "adjoint_gbs": 3 * e.m * s * n * K / ta / 1e6}
 
 
 if want("C1"):
@@ -214,6 +218,9 @@ if want("C5"):
                  "unsteady_node_sweeps_per_s_mlups": e.n * (fs + NT) / dt / 1e6}
     print("C5", json.dumps(out["C5"]), flush=True)
 
+if os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+    with open(os.path.join(ROOT, "gpurun_out", f"{tag}_configs_part.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
 path = os.path.join(ROOT, "profiles", f"{tag}_configs.json")
 old = {}
 if os.path.exists(path):
