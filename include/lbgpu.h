@@ -145,6 +145,23 @@ int lbgpu_get_design_values(lbgpu_engine* e, double* w_design);
 /* n x primal_step (collision.cpp:308-363); residual (nullable) = step_residual
  * of the last step (collision.cpp:365-375). */
 int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual);
+/* tangent_solve (adjoint.cpp:422-490): forward-mode sensitivity of the
+ * objective along a design direction dw (DesignField::nodes order) plus
+ * d_inlet_dp, from the current primal state (frozen base). df starts at zero
+ * and is iterated to max|df_new - df_old| <= tol (solve_fixed_point's stop
+ * rule); dF = sum over the support of dF^x/df . df. "tangent diverged at
+ * iteration k" (LBGPU_E_NUMERIC) on a non-finite residual. iterations,
+ * residual, converged are nullable. Engine state (f, v, w) is unchanged. */
+int lbgpu_tangent_solve(lbgpu_engine* e, const double* dw_design, double d_inlet_dp, double tol,
+                        int64_t max_iter, double* dF, int64_t* iterations, double* residual,
+                        int* converged);
+/* fd_gradient (adjoint.cpp:492-517): central difference (J(p+h) - J(p-h)) / 2h
+ * of the raw objective along design node `ordinal` (DesignField::nodes order;
+ * < 0: inlet_dp), each side a cold-start primal solve to tol / max_iter, or of
+ * exactly fixed_iters steps when fixed_iters >= 0. The perturbation is a raw
+ * write (no clamp), as in the reference. State, design and model are restored. */
+int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, int64_t max_iter,
+                      int64_t fixed_iters, double* out);
 /* optimizer.cpp:200-202: write new design values (DesignField::nodes order,
  * host memory; pinned overlaps best) into w, then n >= 1 primal steps. The
  * upload is pipelined under the first sweep in z-chunks. Equivalent to

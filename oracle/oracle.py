@@ -310,6 +310,9 @@ def _load_ref():
         L.ref_partition_check.argtypes = [vp, C.c_int, C.c_long, C.POINTER(C.c_double),
                                           C.POINTER(C.c_double)]
         L.ref_time.argtypes = [vp, C.c_int, C.c_int, C.c_long, C.POINTER(C.c_double)]
+        L.ref_tangent.argtypes = [vp, vp, C.c_double, C.c_double, C.c_long,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_long),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_int)]
         _rlib = L
     return _rlib
 
@@ -435,6 +438,16 @@ class RefOracle:
         v = C.c_double()
         self._ok(self.L.ref_fd_gradient(self.h, ordinal, step, tol, max_iter, fixed, C.byref(v)))
         return v.value
+
+    def tangent(self, dw, d_inlet_dp, tol, max_iter):
+        """tangent_solve (adjoint.cpp:422-489) from the current primal state:
+        (dF, iterations, residual, converged)."""
+        dw = np.ascontiguousarray(dw, np.float64)
+        dF, r = C.c_double(), C.c_double()
+        it, cv = C.c_long(), C.c_int()
+        self._ok(self.L.ref_tangent(self.h, dw.ctypes.data, d_inlet_dp, tol, max_iter,
+                                    C.byref(dF), C.byref(it), C.byref(r), C.byref(cv)))
+        return dF.value, it.value, r.value, bool(cv.value)
 
     def partition_check(self, parts, steps):
         a, b = C.c_double(), C.c_double()

@@ -304,6 +304,24 @@ int ref_fd_gradient(void* h, long ordinal, double step, double tol, long max_ite
   });
 }
 
+// tangent_solve (adjoint.cpp:422-489) on the current primal state; dw in
+// DesignField::nodes order. out: dF, iterations, residual, converged.
+int ref_tangent(void* h, const double* dw, double d_inlet_dp, double tol, long max_iter,
+                double* dF, long* iters, double* resid, int* conv) {
+  return guard([&] {
+    Direction d;
+    d.dw.assign(dw, dw + H(h)->bc.sys.design.nodes.size());
+    d.d_inlet_dp = d_inlet_dp;
+    std::visit([&](auto& F) {
+      const auto r = tangent_solve(H(h)->bc.sys, H(h)->bc.objective, F.f, d, tol, max_iter);
+      *dF = r.dF;
+      *iters = r.solve.iterations;
+      *resid = r.solve.residual;
+      *conv = r.solve.converged ? 1 : 0;
+    }, H(h)->fl);
+  });
+}
+
 int ref_partition_check(void* h, int parts, long steps, double* pd, double* ad) {
   return guard([&] {
     const PartitionCheckResult r =

@@ -104,6 +104,9 @@ def load_library() -> C.CDLL:
     L.lbgpu_get_design_values.argtypes = [vp, vp]
     L.lbgpu_primal_step.argtypes = [vp, i64, dp]
     L.lbgpu_primal_step_with_design.argtypes = [vp, vp, i64, dp]
+    L.lbgpu_fd_gradient.argtypes = [vp, i64, C.c_double, C.c_double, i64, i64, dp]
+    L.lbgpu_tangent_solve.argtypes = [vp, vp, C.c_double, C.c_double, i64, dp, C.POINTER(i64), dp,
+                                      C.POINTER(C.c_int)]
     L.lbgpu_adjoint_step.argtypes = [vp, i64, C.c_int, dp]
     L.lbgpu_solve_primal.argtypes = [vp, C.c_double, i64, i64, C.POINTER(i64), dp,
                                      C.POINTER(C.c_int)]
@@ -300,6 +303,27 @@ class Engine:
         self._ok(self.L.lbgpu_primal_step_with_design(self.h, _ptr(w_design), n,
                                                       C.byref(r) if residual else None))
         return r.value if residual else None
+
+    def fd_gradient(self, ordinal: int, h: float, tol: float, max_iter: int = 200000,
+                    fixed_iters: int = -1) -> float:
+        """fd_gradient (adjoint.cpp:492-517): ordinal in DesignField::nodes order,
+        < 0 for inlet_dp."""
+        out = C.c_double()
+        self._ok(self.L.lbgpu_fd_gradient(self.h, ordinal, h, tol, max_iter, fixed_iters,
+                                          C.byref(out)))
+        return out.value
+
+    def tangent_solve(self, dw: np.ndarray, d_inlet_dp: float, tol: float,
+                      max_iter: int = 200000) -> tuple[float, int, float, bool]:
+        """tangent_solve (adjoint.cpp:422-490) from the current primal state:
+        (dF, iterations, residual, converged)."""
+        dw = np.ascontiguousarray(dw, np.float64)
+        assert dw.size == self.n_design
+        dF, r = C.c_double(), C.c_double()
+        it, cv = C.c_int64(), C.c_int()
+        self._ok(self.L.lbgpu_tangent_solve(self.h, _ptr(dw), d_inlet_dp, tol, max_iter,
+                                            C.byref(dF), C.byref(it), C.byref(r), C.byref(cv)))
+        return dF.value, it.value, r.value, bool(cv.value)
 
     def design_values(self) -> np.ndarray:
         out = np.empty(max(self.n_design, 1))

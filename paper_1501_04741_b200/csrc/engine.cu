@@ -306,6 +306,11 @@ struct lbgpu_engine {
   void* f[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
   void* snap = nullptr;  // rollback copy for exact tol-stop in batched solves
+  void* tg[2] = {nullptr, nullptr};  // tangent df (post-collision pull layout), lazily
+  int tc = 0;
+  double* d_dw = nullptr;            // tangent direction on the full grid
+  double tangent_drho = 0.0;         // 3 * d_inlet_dp
+  double inlet_dp = 0.0;             // ModelParams::inlet_dp (rho_in = 1 + 3 inlet_dp)
   int fc = 0, vc = 0;
   uint8_t* d_code = nullptr;
   double *d_w = nullptr, *d_bcT = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
@@ -323,7 +328,7 @@ struct lbgpu_engine {
   PairTree tree_support, tree_design, tree_inlet;
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  long long primal_steps = 0, adjoint_steps = 0;
+  long long primal_steps = 0, adjoint_steps = 0, tangent_steps = 0;
   long long launches = 0;  // kernels this engine launched (sweeps + reductions + layout)
   std::vector<cudaEvent_t> evs;  // per-sweep timing events (lbgpu_time_pairs)
   std::string err;
@@ -341,7 +346,8 @@ struct lbgpu_engine {
     if (st_h2d) cudaStreamDestroy(st_h2d);
     for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
-    for (void* p : {f[0], f[1], v[0], v[1], snap}) cudaFree(p);
+    for (void* p : {f[0], f[1], v[0], v[1], snap, tg[0], tg[1]}) cudaFree(p);
+    cudaFree(d_dw);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
     cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals);
@@ -542,6 +548,7 @@ struct lbgpu_engine {
     }
     M.om = om;
     M.beta_f = d.beta_fluid, M.beta_s = d.beta_solid;
+    inlet_dp = d.inlet_dp;
     M.rho_in = 1.0 + 3.0 * d.inlet_dp;
     M.rho_out = 1.0;
     M.u_clamp = d.u_clamp;
@@ -707,6 +714,15 @@ struct lbgpu_engine {
     };
     if (exch && xmode == 2) overlapped(1, dst, s, go);
     else go(s);
+  }
+  // One tangent sweep of df against the frozen primal state f[fc].
+  void tangent_launch(bool resid, unsigned long long* slot) {
+    ++tangent_steps;
+    ++launches;
+    const SweepArgs s = sweep(tangent_steps, resid, slot);
+    if (exact) exact::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
+    else fast::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
+    tc ^= 1;
   }
   void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
     primal_raw(f[fc], f[1 - fc], resid, slot, exch);
@@ -895,7 +911,7 @@ struct lbgpu_engine {
              long long* iters, double* resid, int* conv, bool reset_v = true) {
     require_solo();
     const long long n = fixed >= 0 ? fixed : max_iter;
-    const char* what = which == 0 ? "iteration" : "adjoint iteration";
+    const char* what = which == 0 ? "iteration" : which == 1 ? "adjoint iteration" : "tangent iteration";
     if (which == 1 && reset_v) {
       CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
       CU(cudaMemsetAsync(v[1 - vc], 0, field_bytes(), st));
@@ -907,15 +923,17 @@ struct lbgpu_engine {
     long long batch = 1;
     while (it < n) {
       const long long b = std::min<long long>({batch, n - it, (long long)kRing});
-      void** buf = which == 0 ? f : v;
-      int& cur = which == 0 ? fc : vc;
+      void** buf = which == 0 ? f : which == 1 ? v : tg;
+      int& cur = which == 0 ? fc : which == 1 ? vc : tc;
       const int cur0 = cur;
-      const long long steps0 = which == 0 ? primal_steps : adjoint_steps;
+      long long& steps = which == 0 ? primal_steps : which == 1 ? adjoint_steps : tangent_steps;
+      const long long steps0 = steps;
       if (fixed < 0 && b > 1) CU(cudaMemcpyAsync(snap, buf[cur], field_bytes(), cudaMemcpyDeviceToDevice, st));
       CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long) * b, st));
       for (long long k = 0; k < b; ++k) {
         if (which == 0) primal_launch(true, d_ring + k);
-        else adjoint_launch(kernel, true, d_ring + k);
+        else if (which == 1) adjoint_launch(kernel, true, d_ring + k);
+        else tangent_launch(true, d_ring + k);
       }
       CU(cudaGetLastError());
       reduce_flags(d_ring, size_t(b), false);
@@ -932,6 +950,8 @@ struct lbgpu_engine {
         if (badk) raise_bad(h_flags[1], what);
         if (!std::isfinite(rk)) {
           reset_flags();
+          if (which == 2)  // adjoint.cpp:472-473
+            throw Fail{LBGPU_E_NUMERIC, "tangent diverged at iteration " + std::to_string(itk)};
           throw Fail{LBGPU_E_NUMERIC, std::string(which == 0 ? "state" : "adjoint") +
                                           " diverged (non-finite residual) at iteration " +
                                           std::to_string(itk)};
@@ -946,11 +966,11 @@ struct lbgpu_engine {
         if (stop < b - 1) {  // roll back and replay exactly stop+1 steps
           CU(cudaMemcpyAsync(buf[cur0], snap, field_bytes(), cudaMemcpyDeviceToDevice, st));
           cur = cur0;
-          if (which == 0) primal_steps = steps0;
-          else adjoint_steps = steps0;
+          steps = steps0;
           for (long long k = 0; k <= stop; ++k) {
             if (which == 0) primal_launch(false, nullptr);
-            else adjoint_launch(kernel, false, nullptr);
+            else if (which == 1) adjoint_launch(kernel, false, nullptr);
+            else tangent_launch(false, nullptr);
           }
           sync();
         }
@@ -964,6 +984,100 @@ struct lbgpu_engine {
     *iters = it;
     *resid = r;
     *conv = r <= tol;
+  }
+
+  // tangent_solve (adjoint.cpp:422-490) from the current primal state: df from
+  // zero to its fixed point under the frozen base (the solve() stop rule, same
+  // batching and exact replay), then dF over the support, pairwise-summed.
+  void tangent(const double* dw_design, double d_inlet_dp, double tol, long long max_iter,
+               double* dF, long long* iters, double* resid, int* conv) {
+    require_solo();
+    if (!tg[0]) {
+      CU(cudaMalloc(&tg[0], field_bytes()));
+      CU(cudaMalloc(&tg[1], field_bytes()));
+    }
+    if (!d_dw) CU(cudaMalloc(&d_dw, sizeof(double) * N));
+    CU(cudaMemsetAsync(d_dw, 0, sizeof(double) * N, st));
+    const long long n = (long long)design.size();
+    if (n) {
+      if (!d_wvals) CU(cudaMalloc(&d_wvals, sizeof(double) * n));
+      CU(cudaMemcpyAsync(d_wvals, dw_design, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      k_scatter_design<<<unsigned((n + 255) / 256), 256, 0, st>>>(d_wvals, d_design, n, d_dw);
+      ++launches;
+    }
+    tangent_drho = 3.0 * d_inlet_dp;
+    CU(cudaMemsetAsync(tg[tc], 0, field_bytes(), st));
+    CU(cudaMemsetAsync(tg[1 - tc], 0, field_bytes(), st));
+    solve(2, tol, max_iter, -1, 0, iters, resid, conv);
+    const Launch a = launch(tangent_steps);
+    if (exact) exact::tangent_terms(a, dim, prec, f[fc], tg[tc], d_support, (long long)support.size(), d_terms);
+    else fast::tangent_terms(a, dim, prec, f[fc], tg[tc], d_support, (long long)support.size(), d_terms);
+    CU(cudaGetLastError());
+    *dF = pairwise(tree_support, d_terms);
+  }
+
+  void sync_host_w() {
+    if (!w_host_stale) return;
+    CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    sync();
+    w_host_stale = false;
+  }
+  // Raw write of one node's w (no clamp), with its libm pow pair in exact mode.
+  void set_node_w(long long idx, double val) {
+    w[idx] = val;
+    CU(cudaMemcpyAsync(d_w + idx, &w[idx], sizeof(double), cudaMemcpyHostToDevice, st));
+    if (exact) {
+      const double base = M.fluid_power ? val : 1.0 - val;
+      const double pp[2] = {std::pow(base, M.theta), std::pow(base, M.theta - 1.0)};
+      CU(cudaMemcpyAsync(d_p0 + idx, &pp[0], sizeof(double), cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(d_p1 + idx, &pp[1], sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    sync();
+  }
+  // fd_gradient (adjoint.cpp:492-517): central difference of the raw objective
+  // along design node `ordinal` (DesignField::nodes order) or, for ordinal < 0,
+  // inlet_dp; each side is a cold-start primal solve (tol / max_iter, or
+  // exactly `fixed` steps when fixed >= 0) with the parameter raw-perturbed.
+  // The engine's primal state, design and model are restored afterwards.
+  double fd_gradient(long long ordinal, double h, double tol, long long max_iter, long long fixed) {
+    require_solo();
+    if (ordinal >= (long long)design.size())
+      throw Fail{LBGPU_E_ARG, "design ordinal out of range"};
+    sync_host_w();
+    void* save = nullptr;
+    CU(cudaMalloc(&save, field_bytes()));
+    CU(cudaMemcpyAsync(save, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
+    const int fc0 = fc;
+    const double rho0 = M.rho_in;
+    const long long idx = ordinal >= 0 ? design[ordinal] : -1;
+    const double w0 = idx >= 0 ? w[idx] : 0.0;
+    auto restore = [&] {
+      M.rho_in = rho0;
+      if (idx >= 0) set_node_w(idx, w0);
+      fc = fc0;
+      CU(cudaMemcpyAsync(f[fc], save, field_bytes(), cudaMemcpyDeviceToDevice, st));
+      sync();
+      cudaFree(save);
+    };
+    try {
+      auto run = [&](double delta) {
+        if (idx < 0) M.rho_in = 1.0 + 3.0 * (inlet_dp + delta);  // rho_inlet(), collision.hpp:57
+        else set_node_w(idx, w0 + delta);
+        init_state();
+        long long it = 0;
+        double r = 0.0;
+        int c = 0;
+        solve(0, tol, max_iter, fixed, 0, &it, &r, &c);
+        return objective();
+      };
+      const double fp = run(+h);
+      const double fm = run(-h);
+      restore();
+      return (fp - fm) / (2.0 * h);
+    } catch (...) {
+      try { restore(); } catch (...) {}
+      throw;
+    }
   }
 
   // ------------------------------------------------------- reductions
@@ -1656,6 +1770,27 @@ int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64
     const double r = e->design_steps(w_design, n, residual != nullptr);
     if (residual) *residual = r;
   });
+}
+
+int lbgpu_tangent_solve(lbgpu_engine* e, const double* dw_design, double d_inlet_dp, double tol,
+                        int64_t max_iter, double* dF, int64_t* iterations, double* residual,
+                        int* converged) {
+  if (!dw_design || !dF || max_iter < 0) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    long long it = 0;
+    double r = 0.0;
+    int c = 0;
+    e->tangent(dw_design, d_inlet_dp, tol, max_iter, dF, &it, &r, &c);
+    if (iterations) *iterations = it;
+    if (residual) *residual = r;
+    if (converged) *converged = c;
+  });
+}
+
+int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, int64_t max_iter,
+                      int64_t fixed_iters, double* out) {
+  if (!out || !(h != 0.0)) return LBGPU_E_ARG;
+  return guarded(e, [&] { *out = e->fd_gradient(ordinal, h, tol, max_iter, fixed_iters); });
 }
 
 int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual) {

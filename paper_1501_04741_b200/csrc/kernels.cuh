@@ -975,6 +975,70 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
   if constexpr (UPDATE) block_max_bits(cmax, a.fl.aux);
 }
 
+// Tangent sweep (tangent_solve, adjoint.cpp:438-476): a primal-shaped pull
+// sweep of Dual<R> = (frozen base, df) through the reference-order
+// collide_node with w -> (w, dw) and rho_in -> (rho_in, 3 d_inlet_dp); the
+// derivative part is stored and the residual is step_residual(df). The value
+// part never advances, so only df ping-pongs. Both builds use the reference
+// formulas (a verification path).
+template <class L, class R, bool RESID>
+__global__ void __launch_bounds__(128) k_tangent(Launch a, const R* __restrict__ base,
+                                                 const R* __restrict__ src, R* __restrict__ dst,
+                                                 const double* __restrict__ dw, double d_rho_in) {
+  using namespace detail;
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (x < a.g.x1) {
+    const Geom& g = a.g;
+    const int y = blockIdx.y, z = g.z0 + blockIdx.z;
+    const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+    const Nbr nb = make_nbr(g, x, y, z);
+    R fb[L::M], fd[L::M];
+    gather<L, R, -1>(base, g.N, nb, fb);
+    gather<L, R, -1>(src, g.N, nb, fd);
+    const uint8_t code = a.t.code[idx];
+    const bool hw = code & CODE_HAS_W;
+    const double w = hw ? a.t.w[idx] : 1.0;
+    const double dwv = hw ? dw[idx] : 0.0;
+    const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
+    Dual<R> din[L::M], dout[L::M];
+#pragma unroll
+    for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(fb[k], fd[k]);
+    collide_node<L>(a.M, pp, code & TAG_MASK, code_axis(code), code_sign(code), a.t.bcT[idx], din,
+                    Dual<R>(R(w), R(dwv)), Dual<R>(R(a.M.rho_in), R(d_rho_in)), dout);
+    R out[L::M];
+#pragma unroll
+    for (int k = 0; k < L::M; ++k) out[k] = dout[k].d;
+    store_node<L, R, RESID>(src, dst, g.N, idx, fd, out, rmax);
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
+}
+
+// dF terms of tangent_solve (adjoint.cpp:478-488): per support node,
+// sum_p dF^x/df_p * df_p accumulated in double in plane order.
+template <class L, class R>
+__global__ void k_tangent_terms(Launch a, const R* __restrict__ base, const R* __restrict__ df,
+                                const long long* __restrict__ nodes, long long n,
+                                double* __restrict__ terms) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Geom& g = a.g;
+  const long long idx = nodes[i];
+  const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
+  const Nbr nb = make_nbr(g, x, y, z);
+  R fin[L::M], dfin[L::M], b[L::M];
+  gather<L, R, -1>(base, g.N, nb, fin);
+  gather<L, R, -1>(df, g.N, nb, dfin);
+#pragma unroll
+  for (int k = 0; k < L::M; ++k) b[k] = R(0);
+  node_partial<L, R>(a.M, fin, b);
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < L::M; ++k) acc += double(b[k]) * double(dfin[k]);
+  terms[i] = acc;
+}
+
 // Objective terms F^x on the support list (evaluate_raw, objective.cpp:64-72).
 template <class L, class R>
 __global__ void k_objective_terms(Launch a, const R* __restrict__ p,
@@ -1274,6 +1338,29 @@ void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* 
   const unsigned nb = unsigned((n + 127) / 128);
   LBGPU_LR_DISPATCH(dim, prec, (k_inlet_terms<L, R><<<nb, 128, 0, a.stream>>>(
                                     a, static_cast<const R*>(p), static_cast<const R*>(q),
+                                    nodes, n, terms)));
+}
+#endif
+#if defined(LBGPU_PART_TANGENT)
+void tangent(const SweepArgs& s, const void* base, const void* src, void* dst, const double* dw,
+             double d_rho_in) {
+  const Launch& a = s.a;
+  const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+  dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+  LBGPU_LR_DISPATCH(s.dim, s.prec, {
+    const R* b = static_cast<const R*>(base);
+    const R* in = static_cast<const R*>(src);
+    R* out = static_cast<R*>(dst);
+    if (s.resid) k_tangent<L, R, true><<<grid, bx, 0, a.stream>>>(a, b, in, out, dw, d_rho_in);
+    else k_tangent<L, R, false><<<grid, bx, 0, a.stream>>>(a, b, in, out, dw, d_rho_in);
+  });
+}
+void tangent_terms(const Launch& a, int dim, int prec, const void* base, const void* df,
+                   const long long* nodes, long long n, double* terms) {
+  if (n <= 0) return;
+  const unsigned nb = unsigned((n + 127) / 128);
+  LBGPU_LR_DISPATCH(dim, prec, (k_tangent_terms<L, R><<<nb, 128, 0, a.stream>>>(
+                                    a, static_cast<const R*>(base), static_cast<const R*>(df),
                                     nodes, n, terms)));
 }
 #endif

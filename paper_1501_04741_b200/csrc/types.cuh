@@ -68,6 +68,10 @@ struct SweepArgs {
   void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
               void* out, cudaStream_t st);                                                 \
   void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
+  void tangent(const SweepArgs& s, const void* base, const void* src, void* dst,              \
+               const double* dw, double d_rho_in);                                           \
+  void tangent_terms(const Launch& a, int dim, int prec, const void* base, const void* df,   \
+                     const long long* nodes, long long n, double* terms);                    \
   void halo(int op, const Geom& g, int dim, int prec, int field, void* buf, void* a, void* b, \
             const void* left, const Geom& gl, const void* right, const Geom& gr,             \
             cudaStream_t st);                                                              \

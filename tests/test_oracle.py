@@ -110,3 +110,23 @@ def test_pairwise_sum_tree(oracle_mod):
         mid = lo + (hi - lo) // 2
         return pw(lo, mid) + pw(mid, hi)
     assert s == pw(0, 1000)
+
+
+def test_reference_tangent_is_dual_to_adjoint(oracle_mod):
+    """oracle/_ref's tangent_solve (the reference's own, through ref_shim)
+    reproduces test_adjoint.cpp:173-202 on gradcheck2d: dF == g . dw +
+    g_dp * d_dp within 1e-10 — the pin for the GPU tangent parity tests."""
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_1501_04741_b200.presets import preset_text
+    r = oracle_mod.RefOracle(preset_text("gradcheck2d"))
+    r.init_state()
+    assert r.solve_primal(1e-12, 400000)[2]
+    assert r.solve_adjoint(1e-13, 400000)[2]
+    g, gdp = r.gradient()
+    rng = np.random.default_rng(1)
+    dw = rng.uniform(-1, 1, g.size)
+    ddp = float(rng.uniform(-1, 1))
+    dF, it, res, conv = r.tangent(dw, ddp, 1e-13, 400000)
+    dot = float(g @ dw + gdp * ddp)
+    assert conv and abs(dF - dot) <= 1e-10 * max(1.0, abs(dot))
