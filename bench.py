@@ -226,6 +226,16 @@ def main() -> None:
         t = torch.tensor([ms_tot, ms_p, ms_a], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_tot, ms_p, ms_a = t.tolist()
+    # SURVEY.md §8d C3 protocol for the adjoint alone: the base frozen (the
+    # steady solve_adjoint path, moment cache built once inside the timing)
+    eng.time_sweeps(1, args.warmup)
+    barrier()
+    ms_f = eng.time_sweeps(1, args.steps)
+    barrier()
+    if dist:
+        t = torch.tensor([ms_f], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_f = t.item()
     K = args.steps
     value = world * nodes * K / (ms_tot / 1e3) / 1e6
     primal_mlups = world * nodes * K / (ms_p / 1e3) / 1e6
@@ -247,16 +257,26 @@ def main() -> None:
     # the reference's MMA update produces it, optimizer.cpp:200-202) from
     # pinned host memory and runs one primal sweep — one call,
     # lbgpu_primal_step_with_design, which pipelines the upload under the
-    # sweep — then one adjoint sweep (lbgpu_adjoint_step); each call returns
-    # its step residual to the host.
+    # sweep — then one adjoint sweep (lbgpu_adjoint_step), and reads the
+    # step's result, the objective J of the new state (lbgpu_objective,
+    # evaluate_raw), back to the host. Like the reference's one-shot loop the
+    # sweeps skip the optional step_residual; each call still returns its
+    # status (the rho <= 0 check) synchronously.
     w_host = torch.from_numpy(eng.design_values()).pin_memory()
     w_np = w_host.numpy()
     eng.set_design_values(w_np)
+
+    def e2e_step():
+        eng.primal_step_with_design(w_np, 1, residual=False)
+        eng.adjoint_step(1, residual=False)
+        return eng.objective()
+
+    for _ in range(args.warmup):  # untimed, like the device-timed steps
+        e2e_step()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        eng.primal_step_with_design(w_np, 1)
-        eng.adjoint_step(1)
+        e2e_step()
     torch.cuda.synchronize(local)
     e2e_s = time.perf_counter() - t0
     if dist:
@@ -264,10 +284,11 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
     e2e = {"value": world * nodes * args.e2e_steps / e2e_s / 1e6, "unit": "MLUPS",
-           "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": 16,
+           # J (8 B) + the two calls' status words (4 x 8 B each)
+           "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": 8 + 2 * 32,
            "steps": args.e2e_steps,
-           "path": "lbgpu_primal_step_with_design(pinned host w) + lbgpu_adjoint_step "
-                   "(each returns its residual)"}
+           "path": "lbgpu_primal_step_with_design(pinned host w) + lbgpu_adjoint_step + "
+                   "lbgpu_objective (J to the host)"}
 
     if rank != 0:
         if dist:
@@ -294,6 +315,7 @@ def main() -> None:
                    "l2": "no flush: each sweep streams >= 1.7 GB, 14x the 126 MB L2"},
         "primal_mlups": primal_mlups, "adjoint_mlups": adjoint_mlups,
         "primal_hbm_gbs": ach_p, "adjoint_hbm_gbs": ach_a,
+        "adjoint_frozen_base_mlups": world * nodes * K / (ms_f / 1e3) / 1e6,
         "roofline": {"bound": "hbm", "kernel": "k_adjoint (fast, FMRT, FP64)",
                      "achieved": ach_a, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": ach_a / pk["hbm_gbs"], "traffic": traffic,

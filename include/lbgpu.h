@@ -241,7 +241,9 @@ int lbgpu_one_shot_range(lbgpu_engine* e, int64_t first, int64_t count, int64_t 
 
 /* --- timing (device events on the engine stream; bench support) --- */
 /* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of
- * `steps` back-to-back sweeps (no residual), bracketed by synchronisation. */
+ * `steps` back-to-back sweeps (no residual), bracketed by synchronisation.
+ * Adjoint sweeps run against the frozen current primal state, with its
+ * moment cache built once inside the timed region (the steady-solve path). */
 int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms);
 /* `steps` x (one primal sweep then one adjoint sweep against it), one CUDA
  * event between consecutive sweeps: total, primal-only and adjoint-only ms. */

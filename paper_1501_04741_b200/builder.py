@@ -21,7 +21,10 @@ NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("LBGPU_NVCC_EXTRA", "").split()
 COMMON = [*EXTRA, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-          "--expt-relaxed-constexpr", f"-I{os.path.join(os.path.dirname(HERE), 'include')}"]
+          "--expt-relaxed-constexpr", "-diag-suppress", "20058",
+          f"-I{os.path.join(os.path.dirname(HERE), 'include')}"]
+# 20058: "#pragma unroll must precede a loop" — LBGPU_FOR bodies contain
+# compile-time-unrolled lambdas; the pragmas there are harmless
 
 
 def _sources():

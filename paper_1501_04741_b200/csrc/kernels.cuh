@@ -774,10 +774,11 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 // adjoint.cpp:59, :95); face lanes rebuild / un-build in place. SPLIT leaves
 // the rare side-list nodes (synthetic-objective support, support nodes on a
 // face) to k_adjoint_side.
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
 __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restrict__ base,
                                              const R* __restrict__ src, R* __restrict__ dst,
-                                             int x, int y, int z, unsigned long long& rmax) {
+                                             const R* __restrict__ mom, int x, int y, int z,
+                                             unsigned long long& rmax) {
   using namespace detail;
   const Geom& g = a.g;
   const long long N = g.N;
@@ -786,6 +787,9 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
   const int tag = code & TAG_MASK;
   const bool face = is_face(tag);
   const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
+  if constexpr (MOM) {
+    if (face) return;  // k_adjoint_list: faces gather their base (face_forward)
+  }
   if (!(SPLIT && side)) {
     const Nbr nb = make_nbr(g, x, y, z);
     R vin[L::M], vout[L::M];
@@ -799,7 +803,13 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
       R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
       FaceState<R> fs{};
       const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
-      if (need) {
+      if (need && MOM) {  // frozen base: its moments, cached (k_base_moments)
+        rho = mom[idx];
+        jv[0] = mom[N + idx];
+        jv[1] = mom[2 * N + idx];
+        if constexpr (L::DIM == 3) jv[2] = mom[3 * N + idx];
+        T = mom[(L::DIM + 1) * N + idx];
+      } else if (need) {
         R fin[L::M];
         gather<L, R, -1>(base, N, nb, fin);
         if (face) {
@@ -840,6 +850,40 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
   }
   }
 
+// Moments of a frozen adjoint base (rho, j, T per node: planes 0..DIM+1),
+// computed once per steady adjoint solve: the moment-form VJP reads the base
+// only through them (adjoint.cpp:59, :95), so each sweep then reads
+// (DIM + 2) reals per node instead of gathering all M populations. Same
+// arithmetic as the in-sweep path, so the adjoint states are bitwise equal.
+// Pressure-face nodes are skipped: they gather their base in the sweep.
+template <class L, class R>
+__global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restrict__ base,
+                                                      R* __restrict__ mom) {
+  using namespace detail;
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= a.g.x1) return;
+  const Geom& g = a.g;
+  const int y = blockIdx.y, z = blockIdx.z;
+  const long long N = g.N;
+  const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+  const uint8_t code = a.t.code[idx];
+  const int tag = code & TAG_MASK;
+  const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
+  if (!need || is_face(tag)) return;
+  const Nbr nb = make_nbr(g, x, y, z);
+  R fin[L::M];
+  gather<L, R, -1>(base, N, nb, fin);
+  R rho, jv[3], T = R(0);
+  flow_sums<L, R>(fin, rho, jv);
+#pragma unroll
+  for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
+  mom[idx] = rho;
+  mom[N + idx] = jv[0];
+  mom[2 * N + idx] = jv[1];
+  if constexpr (L::DIM == 3) mom[3 * N + idx] = jv[2];
+  mom[(L::DIM + 1) * N + idx] = T;
+}
+
 // Resident blocks per SM the split adjoint is compiled for (register cap
 // 65536 / (128 * minb)). Measured on B200, C3 adjoint GB/s: FP64 minb 4 best
 // (3 and 2 lower); FP32 4: 4197, 5: 4702, 6: 4950, 8: 5215 (64 regs, 24 B
@@ -850,37 +894,68 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
 #ifndef LBGPU_ADJ_MINB32
 #define LBGPU_ADJ_MINB32 8
 #endif
-#define LBGPU_ADJ_BOUNDS(SPLIT, R) \
-  __launch_bounds__(128, (SPLIT) ? (sizeof(R) == 4 ? LBGPU_ADJ_MINB32 : LBGPU_ADJ_MINB) : 1)
+// The moment-cache variant (MOM) keeps the same bounds: measured FP64 5/6/8
+// blocks 9,941 / 7,775 / 5,746 MLUPS against 10,887 at 4 (126 regs, no spill).
+#ifndef LBGPU_ADJ_MINB_MOM
+#define LBGPU_ADJ_MINB_MOM LBGPU_ADJ_MINB
+#endif
+#ifndef LBGPU_ADJ_MINB32_MOM
+#define LBGPU_ADJ_MINB32_MOM LBGPU_ADJ_MINB32
+#endif
+#define LBGPU_ADJ_BOUNDS(SPLIT, R, MOM)                                                 \
+  __launch_bounds__(128, !(SPLIT) ? 1                                                  \
+                         : (MOM) ? (sizeof(R) == 4 ? LBGPU_ADJ_MINB32_MOM : LBGPU_ADJ_MINB_MOM) \
+                                 : (sizeof(R) == 4 ? LBGPU_ADJ_MINB32 : LBGPU_ADJ_MINB))
 
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R) k_adjoint(Launch a,
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
+__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
                                                                 const R* __restrict__ base,
                                                                 const R* __restrict__ src,
-                                                                R* __restrict__ dst) {
+                                                                R* __restrict__ dst,
+                                                                const R* __restrict__ mom) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (x < a.g.x1)
-    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z,
-                                             rmax);
+    adjoint_body<L, R, CK, AK, RESID, SPLIT, MOM>(a, base, src, dst, mom, x, blockIdx.y,
+                                                  a.g.z0 + blockIdx.z, rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT>
-__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R) k_adjoint_cols(Launch a,
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
+__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
                                                                      const R* __restrict__ base,
                                                                      const R* __restrict__ src,
-                                                                     R* __restrict__ dst, int c0,
-                                                                     int c1) {
+                                                                     R* __restrict__ dst,
+                                                                     const R* __restrict__ mom,
+                                                                     int c0, int c1) {
   const long long yz = (long long)a.g.ny * a.g.nz;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (t < 2 * yz) {
     const long long r = t % yz;
-    adjoint_body<L, R, CK, AK, RESID, SPLIT>(a, base, src, dst, t < yz ? c0 : c1,
-                                             int(r % a.g.ny), int(r / a.g.ny), rmax);
+    adjoint_body<L, R, CK, AK, RESID, SPLIT, MOM>(a, base, src, dst, mom, t < yz ? c0 : c1,
+                                                  int(r % a.g.ny), int(r / a.g.ny), rmax);
   }
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
+}
+
+// Listed nodes through the split (moment-form) path without the moment
+// cache: the pressure-face nodes of a MOM sweep.
+template <class L, class R, int CK, bool RESID>
+__global__ void __launch_bounds__(128) k_adjoint_list(Launch a, const R* __restrict__ base,
+                                                      const R* __restrict__ src,
+                                                      R* __restrict__ dst,
+                                                      const long long* __restrict__ nodes,
+                                                      long long n) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rmax = 0;
+  if (i < n) {
+    int x, y, z;
+    idx_xyz(a.g, nodes[i], x, y, z);
+    adjoint_body<L, R, CK, 0, RESID, true, false>(a, base, src, dst, nullptr, x, y, z, rmax);
+  }
+  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
 // Side-list adjoint nodes with the full (reference-form) node update.
@@ -1231,20 +1306,32 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
   R* out = static_cast<R*>(dst);
   constexpr bool split = !LBGPU_EXACT && AK == 0;
   Launch a = s.a;
-  if (s.part == 2) {
-    const long long n = 2ll * a.g.ny * a.g.nz;
-    k_adjoint_cols<L, R, CK, AK, RES, split><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
-        a, b, in, out, a.g.x0, a.g.x1 - 1);
-  } else {
-    if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
-    if (a.g.x1 > a.g.x0) {
-      const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-      dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
-      k_adjoint<L, R, CK, AK, RES, split><<<grid, bx, 0, a.stream>>>(a, b, in, out);
+  const R* mom = static_cast<const R*>(s.mom);
+  auto go = [&]<bool MOM>() {
+    if (s.part == 2) {
+      const long long n = 2ll * a.g.ny * a.g.nz;
+      k_adjoint_cols<L, R, CK, AK, RES, split, MOM><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
+          a, b, in, out, mom, a.g.x0, a.g.x1 - 1);
+    } else {
+      if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+      if (a.g.x1 > a.g.x0) {
+        const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+        dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+        k_adjoint<L, R, CK, AK, RES, split, MOM><<<grid, bx, 0, a.stream>>>(a, b, in, out, mom);
+      }
     }
+  };
+  if constexpr (split) {
+    if (mom) go.template operator()<true>();
+    else go.template operator()<false>();
+  } else {
+    go.template operator()<false>();
   }
   // side-list nodes go with the full sweep, or with the boundary part so that
   // they are final before a halo is packed
+  if (split && mom && s.n_face_list > 0 && s.part != 1)
+    k_adjoint_list<L, R, CK, RES><<<unsigned((s.n_face_list + 127) / 128), 128, 0, a.stream>>>(
+        s.a, b, in, out, s.face_list, s.n_face_list);
   if (split && s.n_adj_side > 0 && s.part != 1)
     k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
         s.a, b, in, out, s.adj_side, s.n_adj_side);
@@ -1294,6 +1381,12 @@ void primal(const SweepArgs& s, const void* src, void* dst) {
 #if defined(LBGPU_PART_ADJOINT)
 void adjoint(const SweepArgs& s, const void* base, const void* src, void* dst) {
   LBGPU_LR_DISPATCH(s.dim, s.prec, (adjoint_l<L, R, 0>(s, base, src, dst)));
+}
+void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom) {
+  const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+  dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+  LBGPU_LR_DISPATCH(dim, prec, (k_base_moments<L, R><<<grid, bx, 0, a.stream>>>(
+                                    a, static_cast<const R*>(base), static_cast<R*>(mom))));
 }
 #endif
 #if defined(LBGPU_PART_ADJDUAL)

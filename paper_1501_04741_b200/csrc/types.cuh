@@ -50,6 +50,9 @@ struct SweepArgs {
   long long n_adj_side;
   int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
   int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
+  const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
+  const long long* face_list = nullptr;  // pressure-face nodes off the side list (MOM sweeps)
+  long long n_face_list = 0;
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).
@@ -68,6 +71,7 @@ struct SweepArgs {
   void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
               void* out, cudaStream_t st);                                                 \
   void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
+  void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom);         \
   void tangent(const SweepArgs& s, const void* base, const void* src, void* dst,              \
                const double* dw, double d_rho_in);                                           \
   void tangent_terms(const Launch& a, int dim, int prec, const void* base, const void* df,   \

@@ -17,7 +17,17 @@ for prec in precs:
     K = 100
     t, tp, ta = e.time_pairs(K)
     s = prec // 8
+    e.adjoint_step(10, residual=False)
+    import torch
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    e.adjoint_step(K, residual=False)
+    tf = (time.perf_counter() - t0) * 1e3
     print(json.dumps({"lib": os.environ.get("LBGPU_LIB", "default"), "prec": prec,
                       "primal_gbs": round(2 * e.m * s * e.n * K / tp / 1e6, 1),
-                      "adjoint_gbs": round(3 * e.m * s * e.n * K / ta / 1e6, 1)}))
+                      "adjoint_gbs": round(3 * e.m * s * e.n * K / ta / 1e6, 1),
+                      "adjoint_mlups": round(e.n * K / ta / 1e3, 1),
+                      "frozen_base_adjoint_mlups": round(e.n * K / tf / 1e3, 1),
+                      "frozen_base_adjoint_gbs": round((2 * e.m + 5) * s * e.n * K / tf / 1e6, 1)}))
     e.close()
