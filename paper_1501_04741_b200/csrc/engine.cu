@@ -301,7 +301,7 @@ struct lbgpu_engine {
   std::vector<uint8_t> tag, mask, code;
   std::vector<double> w, bc_T, A, relax;
   std::vector<int8_t> bc_axis, bc_sign;
-  std::vector<long long> design, support, inlets, adj_side, grad_side, face_list;
+  std::vector<long long> design, support, inlets, adj_side, grad_side;
   // device
   void* f[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -309,7 +309,7 @@ struct lbgpu_engine {
   void* tg[2] = {nullptr, nullptr};  // tangent df (post-collision pull layout), lazily
   int tc = 0;
   double* d_dw = nullptr;            // tangent direction on the full grid
-  void* d_mom = nullptr;             // moments of a frozen adjoint base (k_base_moments)
+  void* d_mom = nullptr;             // frozen adjoint base: moments + face scalars (k_base_moments)
   const void* mom_base = nullptr;    // the base d_mom currently describes (inside a scope)
   double tangent_drho = 0.0;         // 3 * d_inlet_dp
   double inlet_dp = 0.0;             // ModelParams::inlet_dp (rho_in = 1 + 3 inlet_dp)
@@ -320,7 +320,6 @@ struct lbgpu_engine {
   long long *d_design = nullptr, *d_support = nullptr, *d_inlets = nullptr;
   long long* d_adj_side = nullptr;
   long long* d_grad_side = nullptr;
-  long long* d_face_list = nullptr;
   double *d_terms = nullptr, *d_grad = nullptr, *d_scalar = nullptr;
   double* d_ref = nullptr;
   double* d_wvals = nullptr;  // staging for design-order uploads
@@ -353,7 +352,7 @@ struct lbgpu_engine {
     cudaFree(d_dw), cudaFree(d_mom);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
-    cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_face_list), cudaFree(d_wvals);
+    cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -472,12 +471,6 @@ struct lbgpu_engine {
     for (long long i : support)
       if (M.obj_kind == 2 || tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) adj_side.push_back(i);
     up_list(adj_side, d_adj_side);
-    // pressure-face nodes not on the side list: a MOM sweep's k_adjoint_list
-    for (long long i = 0; i < N; ++i)
-      if ((tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) && (i % nx) < span &&
-          !std::binary_search(support.begin(), support.end(), i))
-        face_list.push_back(i);
-    up_list(face_list, d_face_list);
     // design positions on non-Interior nodes: the gradient's dual side launch
     for (size_t i = 0; i < design.size(); ++i)
       if (tag[design[i]] != TAG_INTERIOR) grad_side.push_back((long long)i);
@@ -712,10 +705,7 @@ struct lbgpu_engine {
     ++adjoint_steps;
     ++launches;
     SweepArgs s = sweep(adjoint_steps, resid, slot);
-    if (kernel == 0 && mom_base && mom_base == base) {
-      s.mom = d_mom;
-      s.face_list = d_face_list, s.n_face_list = (long long)face_list.size();
-    }
+    if (kernel == 0 && mom_base && mom_base == base) s.mom = d_mom;
     auto go = [&](const SweepArgs& a) {
       if (kernel) {
         if (exact) exact::adjoint_dual(a, base, src, dst);
@@ -822,7 +812,7 @@ struct lbgpu_engine {
     lbgpu_engine* e;
     MomScope(lbgpu_engine* e_, long long n, int kernel) : e(e_) {
       if (e->exact || kernel != 0 || n < 2) return;
-      if (!e->d_mom) CU(cudaMalloc(&e->d_mom, e->bytes_per_real() * size_t(e->dim + 2) * e->N));
+      if (!e->d_mom) CU(cudaMalloc(&e->d_mom, e->bytes_per_real() * size_t(e->dim + 7) * e->N));
       fast::base_moments(e->launch(e->adjoint_steps), e->dim, e->prec, e->f[e->fc], e->d_mom);
       CU(cudaGetLastError());
       ++e->launches;

@@ -787,9 +787,6 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
   const int tag = code & TAG_MASK;
   const bool face = is_face(tag);
   const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
-  if constexpr (MOM) {
-    if (face) return;  // k_adjoint_list: faces gather their base (face_forward)
-  }
   if (!(SPLIT && side)) {
     const Nbr nb = make_nbr(g, x, y, z);
     R vin[L::M], vout[L::M];
@@ -809,6 +806,13 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         jv[1] = mom[2 * N + idx];
         if constexpr (L::DIM == 3) jv[2] = mom[3 * N + idx];
         T = mom[(L::DIM + 1) * N + idx];
+        if (face) {  // and the face reconstruction's scalars
+          const R* fp = mom + (L::DIM + 2) * N + idx;
+          fs.ua = fp[0], fs.rho = fp[N], fs.Tstar = fp[2 * N], fs.tden = fp[3 * N];
+          fs.clamped = fp[4 * N] != R(0);
+          fs.rho_t = R(tag == TAG_INLET ? a.M.rho_in : a.M.rho_out);
+          fs.Ksum = R(0);
+        }
       } else if (need) {
         R fin[L::M];
         gather<L, R, -1>(base, N, nb, fin);
@@ -855,7 +859,8 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
 // only through them (adjoint.cpp:59, :95), so each sweep then reads
 // (DIM + 2) reals per node instead of gathering all M populations. Same
 // arithmetic as the in-sweep path, so the adjoint states are bitwise equal.
-// Pressure-face nodes are skipped: they gather their base in the sweep.
+// Pressure-face nodes store the moments of their reconstructed populations
+// and the five scalars face_reverse needs (planes DIM+2 .. DIM+6).
 template <class L, class R>
 __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restrict__ base,
                                                       R* __restrict__ mom) {
@@ -869,10 +874,21 @@ __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restr
   const uint8_t code = a.t.code[idx];
   const int tag = code & TAG_MASK;
   const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
-  if (!need || is_face(tag)) return;
+  if (!need) return;
   const Nbr nb = make_nbr(g, x, y, z);
   R fin[L::M];
   gather<L, R, -1>(base, N, nb, fin);
+  if (is_face(tag)) {
+    FaceState<R> fs;
+    const bool inlet = tag == TAG_INLET;
+    const double bcT = a.t.bcT[idx];
+    face_dispatch<L>(code, [&]<int AX, int SG>() {
+      fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, fin);
+    });
+    R* fp = mom + (L::DIM + 2) * N + idx;
+    fp[0] = fs.ua, fp[N] = fs.rho, fp[2 * N] = fs.Tstar, fp[3 * N] = fs.tden;
+    fp[4 * N] = fs.clamped ? R(1) : R(0);
+  }
   R rho, jv[3], T = R(0);
   flow_sums<L, R>(fin, rho, jv);
 #pragma unroll
@@ -937,25 +953,6 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
                                                   int(r % a.g.ny), int(r / a.g.ny), rmax);
   }
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
-}
-
-// Listed nodes through the split (moment-form) path without the moment
-// cache: the pressure-face nodes of a MOM sweep.
-template <class L, class R, int CK, bool RESID>
-__global__ void __launch_bounds__(128) k_adjoint_list(Launch a, const R* __restrict__ base,
-                                                      const R* __restrict__ src,
-                                                      R* __restrict__ dst,
-                                                      const long long* __restrict__ nodes,
-                                                      long long n) {
-  using namespace detail;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long rmax = 0;
-  if (i < n) {
-    int x, y, z;
-    idx_xyz(a.g, nodes[i], x, y, z);
-    adjoint_body<L, R, CK, 0, RESID, true, false>(a, base, src, dst, nullptr, x, y, z, rmax);
-  }
-  if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
 // Side-list adjoint nodes with the full (reference-form) node update.
@@ -1329,9 +1326,6 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
   }
   // side-list nodes go with the full sweep, or with the boundary part so that
   // they are final before a halo is packed
-  if (split && mom && s.n_face_list > 0 && s.part != 1)
-    k_adjoint_list<L, R, CK, RES><<<unsigned((s.n_face_list + 127) / 128), 128, 0, a.stream>>>(
-        s.a, b, in, out, s.face_list, s.n_face_list);
   if (split && s.n_adj_side > 0 && s.part != 1)
     k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
         s.a, b, in, out, s.adj_side, s.n_adj_side);

@@ -51,8 +51,6 @@ struct SweepArgs {
   int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
   int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
   const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
-  const long long* face_list = nullptr;  // pressure-face nodes off the side list (MOM sweeps)
-  long long n_face_list = 0;
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).
