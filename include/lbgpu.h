@@ -83,6 +83,8 @@ typedef struct {
 } lbgpu_run_row;
 
 const char* lbgpu_version(void);
+/* Visible CUDA devices (0 when there is no usable driver / GPU). */
+int lbgpu_device_count(void);
 /* Local column count of a slab of `span` owned columns (span + 2 ghosts,
  * rounded up to 16 so rows stay 128-byte aligned). */
 int lbgpu_slab_nxl(int span);
@@ -218,6 +220,12 @@ int lbgpu_unsteady_adjoint(lbgpu_engine* e, int64_t n_steps, int sum_objective, 
  * share one stream and step in lock step through the lbgpu_group_* calls,
  * each sweep followed by the halo exchange (neighbour buffers read directly). */
 int lbgpu_group_link(lbgpu_engine** engines, int n);
+/* P2P group: engines[i] is slab i of n >= 2 and may sit on any device (peer
+ * access is enabled between neighbouring GPUs; LBGPU_E_CONFIG without it).
+ * Each keeps its own stream; a sweep writes the planes crossing each cut
+ * straight into the neighbour's ghost column (peer stores over NVLink) and
+ * waits only on its two neighbours' previous sweep. Same lbgpu_group_* calls. */
+int lbgpu_group_link_p2p(lbgpu_engine** engines, int n);
 /* which: 0 primal, 1 adjoint (kernel as lbgpu_adjoint_step); residual =
  * global max-norm step residual of the last step (nullable). */
 int lbgpu_group_step(lbgpu_engine** engines, int n, int which, int64_t steps, int kernel,

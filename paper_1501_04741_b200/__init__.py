@@ -123,6 +123,7 @@ def load_library() -> C.CDLL:
                                                 C.c_int, C.POINTER(vp)]
     L.lbgpu_slab_info.argtypes = [vp, C.POINTER(C.c_int)]
     L.lbgpu_group_link.argtypes = [C.POINTER(vp), C.c_int]
+    L.lbgpu_group_link_p2p.argtypes = [C.POINTER(vp), C.c_int]
     L.lbgpu_group_step.argtypes = [C.POINTER(vp), C.c_int, C.c_int, i64, C.c_int, dp]
     L.lbgpu_group_exchange.argtypes = [C.POINTER(vp), C.c_int, C.c_int]
     L.lbgpu_nccl_unique_id.argtypes = [vp, C.c_int]
@@ -425,19 +426,32 @@ def nccl_unique_id() -> bytes:
 
 
 class SlabGroup:
-    """In-process lock-step group of slab engines on one device (the
-    PartitionedRun of partition.cpp:43-312, with the halo exchange done by a
-    kernel that reads the neighbour slabs' buffers)."""
+    """In-process lock-step group of slab engines: the PartitionedRun of
+    partition.cpp:43-312.
+
+    transport "pull": one device, one shared stream, the halo exchange done by
+    a kernel that reads the neighbour slabs' buffers after each sweep.
+    transport "p2p": one stream per slab, slabs on `devices` (round robin;
+    default all on `device`); each sweep stores its boundary planes straight
+    into the neighbours' ghost columns (peer memory across GPUs) and waits only
+    on its two neighbours' previous sweep."""
 
     def __init__(self, cfg_text: str, overrides: dict | None, n: int, device: int = 0,
-                 exact: bool = False):
-        self.engines = [Engine.slab_from_config(cfg_text, overrides, n, i, device, exact)
-                        for i in range(n)]
+                 exact: bool = False, transport: str = "pull", devices=None):
+        devs = list(devices) if devices else [device]
+        self.engines = [Engine.slab_from_config(cfg_text, overrides, n, i, devs[i % len(devs)],
+                                                exact) for i in range(n)]
         self.L = load_library()
         self._arr = (C.c_void_p * n)(*[e.h.value for e in self.engines])
-        rc = self.L.lbgpu_group_link(self._arr, n)
+        if transport == "p2p" and n > 1:
+            rc = self.L.lbgpu_group_link_p2p(self._arr, n)
+        elif transport in ("pull", "p2p"):
+            rc = self.L.lbgpu_group_link(self._arr, n)
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
         if rc:
-            raise LbgpuError(rc, "lbgpu_group_link failed")
+            raise LbgpuError(rc, self.L.lbgpu_error_message(self._arr[0]).decode()
+                             or "lbgpu_group_link failed")
         self.n = n
         self.slabs = [e.slab() for e in self.engines]
         e0 = self.engines[0]

@@ -280,8 +280,14 @@ struct lbgpu_engine {
   int gnx = 0, x0 = 0, span = 0, slab_count = 1, slab_id = 0;
   bool ghosts = false;  // ghost-column layout (always with >1 slab; one slab on request)
   // halo exchange: 0 none (one slab, periodic wrap), 1 in-process group
-  // (neighbour buffers read directly), 2 NCCL (one slab per rank)
+  // (neighbour buffers read directly), 2 NCCL (one slab per rank), 3
+  // in-process P2P group (one stream per slab, any devices; the sweeps push
+  // their boundary planes into the neighbours' ghosts)
   int xmode = 0;
+  void* push_dst_l = nullptr;  // xmode 3: this sweep's neighbour destinations
+  void* push_dst_r = nullptr;
+  cudaEvent_t ev_step[2] = {nullptr, nullptr};  // xmode 3: sweep k done (parity k)
+  long long gstep = 0;
   lbgpu_engine* nb_left = nullptr;
   lbgpu_engine* nb_right = nullptr;
   ncclComm_t comm = nullptr;
@@ -342,6 +348,8 @@ struct lbgpu_engine {
     if (!st) return;  // host-only instance (lbgpu_case_tables)
     if (comm) nccl().CommDestroy(comm);
     if (ev_bnd) cudaEventDestroy(ev_bnd);
+    for (cudaEvent_t ev : ev_step)
+      if (ev) cudaEventDestroy(ev);
     if (ev_halo) cudaEventDestroy(ev_halo);
     if (st_comm) cudaStreamDestroy(st_comm);
     for (cudaEvent_t ev : ev_chunk) cudaEventDestroy(ev);
@@ -691,7 +699,8 @@ struct lbgpu_engine {
   void primal_raw(const void* src, void* dst, bool resid, unsigned long long* slot, bool exch) {
     ++primal_steps;
     ++launches;
-    const SweepArgs s = sweep(primal_steps, resid, slot);
+    SweepArgs s = sweep(primal_steps, resid, slot);
+    s.a.push = push_targets();
     auto go = [&](const SweepArgs& a) {
       if (exact) exact::primal(a, src, dst);
       else fast::primal(a, src, dst);
@@ -705,6 +714,7 @@ struct lbgpu_engine {
     ++adjoint_steps;
     ++launches;
     SweepArgs s = sweep(adjoint_steps, resid, slot);
+    s.a.push = push_targets();
     if (kernel == 0 && mom_base && mom_base == base) s.mom = d_mom;
     auto go = [&](const SweepArgs& a) {
       if (kernel) {
@@ -726,6 +736,13 @@ struct lbgpu_engine {
     if (exact) exact::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
     else fast::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
     tc ^= 1;
+  }
+  Push push_targets() const {
+    Push p;
+    if (xmode != 3) return p;
+    p.l_dst = push_dst_l, p.l_col = nb_left->span, p.l_nx = nb_left->nx, p.l_N = nb_left->N;
+    p.r_dst = push_dst_r, p.r_col = nb_right->nx - 1, p.r_nx = nb_right->nx, p.r_N = nb_right->N;
+    return p;
   }
   void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
     primal_raw(f[fc], f[1 - fc], resid, slot, exch);
@@ -791,7 +808,7 @@ struct lbgpu_engine {
     if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + nccl().GetErrorString(r)};
   }
   void require_solo() const {
-    if (xmode == 1)
+    if (xmode == 1 || xmode == 3)
       throw Fail{LBGPU_E_STATE, "slab engine in an in-process group: use lbgpu_group_* calls"};
   }
 
@@ -1385,6 +1402,15 @@ extern "C" {
 
 const char* lbgpu_version(void) { return "0.1.0-b200"; }
 
+int lbgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int lbgpu_slab_nxl(int span) { return (span + 2 + 15) / 16 * 16; }
 
 int lbgpu_slab_info(const lbgpu_engine* e, int* out6) {
@@ -1416,18 +1442,114 @@ int lbgpu_group_link(lbgpu_engine** es, int n) {
   return LBGPU_OK;
 }
 
-int lbgpu_group_exchange(lbgpu_engine** es, int n, int field) {
-  if (!es || n < 1 || (field != 0 && field != 1)) return LBGPU_E_ARG;
+// The P2P group (partition.cpp:43-312's PartitionedRun, one stream per slab,
+// slabs on any devices): every sweep stores its boundary planes straight into
+// the neighbours' ghost columns (push_halo, peer memory across GPUs); sweep k
+// of a slab waits only on its two neighbours' sweep k-1 (cross-device events).
+int lbgpu_group_link_p2p(lbgpu_engine** es, int n) {
+  if (!es || n < 2) return LBGPU_E_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!es[i] || es[i]->slab_count != n || es[i]->slab_id != i || !es[i]->ghosts ||
+        es[i]->xmode != 0)
+      return LBGPU_E_ARG;
   for (int i = 0; i < n; ++i) {
-    const int rc = guarded(es[i], [&] { es[i]->exchange(field); });
+    lbgpu_engine* e = es[i];
+    const int rc = guarded(e, [&] {
+      for (lbgpu_engine* nb : {es[(i - 1 + n) % n], es[(i + 1) % n]}) {
+        if (nb->device == e->device) continue;
+        int can = 0;
+        CU(cudaDeviceCanAccessPeer(&can, e->device, nb->device));
+        if (!can)
+          throw Fail{LBGPU_E_CONFIG, "no peer access from GPU " + std::to_string(e->device) +
+                                         " to GPU " + std::to_string(nb->device)};
+        const cudaError_t r = cudaDeviceEnablePeerAccess(nb->device, 0);
+        if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled) CU(r);
+        (void)cudaGetLastError();
+      }
+      for (cudaEvent_t& ev : e->ev_step)
+        if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      e->sync();
+    });
     if (rc) return rc;
   }
-  return guarded(es[0], [&] { es[0]->sync(); });
+  for (int i = 0; i < n; ++i) {
+    es[i]->xmode = 3;
+    es[i]->gstep = 0;
+    es[i]->nb_left = es[(i - 1 + n) % n];
+    es[i]->nb_right = es[(i + 1) % n];
+  }
+  return LBGPU_OK;
+}
+
+int lbgpu_group_exchange(lbgpu_engine** es, int n, int field) {
+  if (!es || n < 1 || (field != 0 && field != 1)) return LBGPU_E_ARG;
+  const bool p2p = es[0]->xmode == 3;
+  if (p2p)  // every slab's buffers final before anyone reads across a cut
+    for (int i = 0; i < n; ++i) {
+      const int rc = guarded(es[i], [&] { es[i]->sync(); });
+      if (rc) return rc;
+    }
+  for (int i = 0; i < n; ++i) {
+    const int rc = guarded(es[i], [&] {
+      if (p2p) es[i]->halo_op(2, field, nullptr, nullptr, es[i]->nb_left, es[i]->nb_right);
+      else es[i]->exchange(field);
+    });
+    if (rc) return rc;
+  }
+  for (int i = 0; i < (p2p ? n : 1); ++i) {
+    const int rc = guarded(es[i], [&] { es[i]->sync(); });
+    if (rc) return rc;
+  }
+  return LBGPU_OK;
 }
 
 int lbgpu_group_step(lbgpu_engine** es, int n, int which, int64_t steps, int kernel,
                      double* residual) {
   if (!es || n < 1 || steps < 0 || (which != 0 && which != 1)) return LBGPU_E_ARG;
+  if (n > 1 && es[0] && es[0]->xmode == 3) {
+    for (int i = 0; i < n; ++i)
+      if (!es[i] || es[i]->xmode != 3) return LBGPU_E_STATE;
+    return guarded(es[0], [&] {
+      for (int i = 0; i < n; ++i) {  // whatever each slab had queued (uploads, init) lands first
+        CU(cudaSetDevice(es[i]->device));
+        es[i]->reset_flags();
+        es[i]->sync();
+      }
+      for (int64_t k = 0; k < steps; ++k) {
+        const bool r = residual && k == steps - 1;
+        // lock step: every slab holds the same buffer parity before sweep k
+        const int par = which == 0 ? es[0]->fc : es[0]->vc;
+        for (int i = 0; i < n; ++i) {
+          lbgpu_engine* e = es[i];
+          CU(cudaSetDevice(e->device));
+          void** nl = which == 0 ? e->nb_left->f : e->nb_left->v;
+          void** nr = which == 0 ? e->nb_right->f : e->nb_right->v;
+          e->push_dst_l = nl[1 - par];
+          e->push_dst_r = nr[1 - par];
+          // neighbours' sweep k-1: their ghosts are read-complete (WAR) and
+          // the planes they pushed into mine are written (RAW)
+          const int prev = int((e->gstep + 1) & 1);
+          CU(cudaStreamWaitEvent(e->st, e->nb_left->ev_step[prev], 0));
+          CU(cudaStreamWaitEvent(e->st, e->nb_right->ev_step[prev], 0));
+          if (which == 0) e->primal_launch(r, nullptr, false);
+          else e->adjoint_launch(kernel, r, nullptr, false);
+          CU(cudaEventRecord(e->ev_step[e->gstep & 1], e->st));
+        }
+        for (int i = 0; i < n; ++i) ++es[i]->gstep;
+      }
+      CU(cudaGetLastError());
+      double rmax = 0.0;
+      for (int i = 0; i < n; ++i) {
+        CU(cudaSetDevice(es[i]->device));
+        es[i]->pull_flags();
+        if (es[i]->h_flags[1] != kNoBad)
+          es[i]->raise_bad(es[i]->h_flags[1], which == 0 ? "iteration" : "adjoint iteration");
+        const double ri = lbgpu_engine::bits_to_double(es[i]->h_flags[0]);
+        if (!(ri <= rmax)) rmax = ri;
+      }
+      if (residual) *residual = rmax;
+    });
+  }
   for (int i = 0; i < n; ++i)
     if (!es[i] || (n > 1 && es[i]->xmode != 1)) return LBGPU_E_STATE;
   return guarded(es[0], [&] {

@@ -705,6 +705,19 @@ struct lbopt_case {
     if (best_obj) *best_obj = bobj;
   }
 
+  // workers -> GPUs: worker i runs on device
+  // (LBOPT_GPU_DEVICE + i) mod G, G = LBOPT_GPU_COUNT or every visible GPU;
+  // the slabs form a P2P group (peer stores across GPUs, concurrent streams
+  // when several share one).
+  static int worker_device(int i) {
+    const int d0 = env_int("LBOPT_GPU_DEVICE", 0);
+    int g = env_int("LBOPT_GPU_COUNT", 0);
+    const int vis = lbgpu_device_count();
+    if (g <= 0 || g > vis) g = vis;
+    if (g <= 0) return d0;
+    return (d0 + i) % g;
+  }
+
   // partition_check (partition.cpp:314-357) against the engine's slab groups.
   void partition_check(long steps, double* max_diff) {
     const std::string text = lbgpu::serialize_case(cfg);
@@ -716,12 +729,13 @@ struct lbopt_case {
       lbgpu_destroy(mono);
     };
     try {
-      const int dev = env_int("LBOPT_GPU_DEVICE", 0), ex = env_int("LBOPT_GPU_EXACT", 0);
+      const int ex = env_int("LBOPT_GPU_EXACT", 0);
       for (int i = 0; i < W; ++i) {
-        const int rc = lbgpu_create_slab_from_config(text.c_str(), "", dev, ex && cfg.precision == 64, W, i, &slabs[i]);
+        const int rc = lbgpu_create_slab_from_config(text.c_str(), "", worker_device(i),
+                                                     ex && cfg.precision == 64, W, i, &slabs[i]);
         if (rc) fail(rc, lbgpu_last_create_error());
       }
-      if (W > 1) ok(slabs[0], lbgpu_group_link(slabs.data(), W));
+      if (W > 1) ok(slabs[0], lbgpu_group_link_p2p(slabs.data(), W));
       std::vector<int> geo(6 * W);
       for (int i = 0; i < W; ++i) lbgpu_slab_info(slabs[i], geo.data() + 6 * i);
       auto gathered = [&](int field) {
@@ -795,10 +809,10 @@ struct lbopt_case {
       };
       try {
         for (int i = 0; i < W; ++i) {
-          const int rc = lbgpu_create_slab_from_config(text.c_str(), "", env_int("LBOPT_GPU_DEVICE", 0), 0, W, i, &slabs[i]);
+          const int rc = lbgpu_create_slab_from_config(text.c_str(), "", worker_device(i), 0, W, i, &slabs[i]);
           if (rc) fail(rc, lbgpu_last_create_error());
         }
-        ok(slabs[0], lbgpu_group_link(slabs.data(), W));
+        ok(slabs[0], W > 1 ? lbgpu_group_link_p2p(slabs.data(), W) : lbgpu_group_link(slabs.data(), W));
         using clk = std::chrono::steady_clock;
         const auto t0 = clk::now();
         ok(slabs[0], lbgpu_group_step(slabs.data(), W, 0, steps, 0, nullptr));

@@ -100,6 +100,49 @@ __device__ __forceinline__ void gather_async(const R* __restrict__ buf, long lon
   cp_async_commit();
 }
 
+// Planes that cross a slab cut for a sweep pulling along D (-1 primal, +1
+// adjoint): side S = -1 are pulled from the left neighbour (D*e_x == -1), S =
+// +1 from the right one; the adjoint's lists are the primal's swapped, the
+// reference's transposed plan (partition.cpp:143-146).
+template <class L, int D, int S>
+__device__ __forceinline__ constexpr int halo_slot(int k) {
+  int c = 0;
+  for (int p = 0; p < L::M; ++p)
+    if (D * cvel<L>(p, 0) == S) {
+      if (c == k) return p;
+      ++c;
+    }
+  return -1;
+}
+template <class L>
+constexpr int kHaloPlanes = 6;  // D2Q9+D2Q9: 3+3, D3Q19+D3Q7: 5+1
+
+// Fused P2P halo: a lane on the slab's first / last owned column also stores
+// the planes its neighbour will pull across the cut straight into that
+// neighbour's destination ghost column (peer memory when the neighbour lives
+// on another GPU). No pack, no separate exchange kernel.
+template <class L, class R, int D>
+__device__ __forceinline__ void push_halo(const Launch& a, int x, int y, int z, const R* out) {
+  const Push& h = a.push;
+  const long long row = y + (long long)a.g.ny * z;
+  if (h.r_dst && x == a.g.x1 - 1) {  // my last column -> right neighbour's left ghost
+    R* d = static_cast<R*>(h.r_dst);
+    const long long i = (long long)h.r_nx * row + h.r_col;
+    LBGPU_FOR(K, 0, kHaloPlanes<L>, {
+      constexpr int p = halo_slot<L, D, -1>(K);
+      d[p * h.r_N + i] = out[p];
+    });
+  }
+  if (h.l_dst && x == a.g.x0) {  // my first column -> left neighbour's right ghost
+    R* d = static_cast<R*>(h.l_dst);
+    const long long i = (long long)h.l_nx * row + h.l_col;
+    LBGPU_FOR(K, 0, kHaloPlanes<L>, {
+      constexpr int p = halo_slot<L, D, +1>(K);
+      d[p * h.l_N + i] = out[p];
+    });
+  }
+}
+
 __device__ __forceinline__ unsigned long long absdiff_bits(double a, double b) {
   return (unsigned long long)__double_as_longlong(fabs(a - b));
 }
@@ -631,6 +674,8 @@ __device__ __forceinline__ void face_dispatch(uint8_t code, F&& fn) {
 }
 
 }  // namespace detail
+using detail::halo_slot;
+using detail::kHaloPlanes;
 
 namespace detail {
 
@@ -761,6 +806,7 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* __restrict
   if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
     atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
   store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
+  push_halo<L, R, -1>(a, x, y, z, out);
 }
 
 // Plain bounds: ptxas picks 64 regs (FP32) / 96-122 (FP64), no spills. Forcing
@@ -890,6 +936,7 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
     }
     if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
     store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
+    push_halo<L, R, +1>(a, x, y, z, vout);
   }
   }
 
@@ -1016,6 +1063,7 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
     if (!adjoint_node_full<L, R, CK, 0>(a, idx, a.t.code[idx], fin, vin, vout))
       atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
     store_node<L, R, RESID>(src, dst, g.N, idx, vin, vout, rmax);
+    push_halo<L, R, +1>(a, x, y, z, vout);
   }
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
@@ -1250,18 +1298,6 @@ __global__ void k_init(long long N, R* __restrict__ buf) {
 // D*e_x = +1 planes to the left neighbour: 6 planes x ny x nz each way for
 // both lattice pairs. For the adjoint (D = +1) these are the primal's lists
 // swapped, the reference's transposed plan (partition.cpp:143-146).
-template <class L, int D, int S>
-__device__ __forceinline__ constexpr int halo_slot(int k) {
-  int c = 0;
-  for (int p = 0; p < L::M; ++p)
-    if (D * cvel<L>(p, 0) == S) {
-      if (c == k) return p;
-      ++c;
-    }
-  return -1;
-}
-template <class L>
-constexpr int kHaloPlanes = 6;  // D2Q9+D2Q9: 3+3, D3Q19+D3Q7: 5+1
 
 template <class L, class R, int D>
 __global__ void k_halo_pack(Geom g, const R* __restrict__ buf, R* __restrict__ send_left,

@@ -34,7 +34,18 @@ struct Flags {
   unsigned long long step_key;  // (step number << 40): orders "bad" reports by step
 };
 
+// P2P halo push targets (in-process slab groups linked with
+// lbgpu_group_link_p2p): the neighbours' destination buffers of this sweep,
+// possibly on other devices (peer memory), and where their ghost columns sit.
+struct Push {
+  void* l_dst = nullptr;  // left neighbour: its right ghost column l_col
+  void* r_dst = nullptr;  // right neighbour: its left ghost column r_col
+  int l_col = 0, l_nx = 0, r_col = 0, r_nx = 0;
+  long long l_N = 0, r_N = 0;
+};
+
 struct Launch {
+  Push push;
   Geom g;
   NodeTables t;
   Model M;

@@ -14,10 +14,14 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("name", ["grad2d", "exch2d", "mix3d", "exch3d", "periodic2d"])
 @pytest.mark.parametrize("parts", [2, 3, 4])
 @pytest.mark.parametrize("exact", [False, True])
-def test_slabs_bitwise_equal_monolithic(lbgpu, has_gpu, name, parts, exact):
+@pytest.mark.parametrize("transport", ["pull", "p2p"])
+def test_slabs_bitwise_equal_monolithic(lbgpu, has_gpu, name, parts, exact, transport):
+    """transport "p2p": one stream per slab, running concurrently; every sweep
+    pushes its boundary planes into the neighbours' ghost columns (the
+    multi-GPU peer-store path, here with all slabs on one device)."""
     txt = case_text(name)
     mono = lbgpu.Engine.from_config(txt, exact=exact)
-    grp = lbgpu.SlabGroup(txt, None, parts, exact=exact)
+    grp = lbgpu.SlabGroup(txt, None, parts, exact=exact, transport=transport)
     mono.init_state()
     grp.init_state()
     r_m = mono.primal_step(30)
@@ -34,10 +38,11 @@ def test_slabs_bitwise_equal_monolithic(lbgpu, has_gpu, name, parts, exact):
     assert np.array_equal(g_g, g_m) and gdp_g == gdp_m
 
 
-def test_slab_upload_round_trip(lbgpu, has_gpu):
+@pytest.mark.parametrize("transport", ["pull", "p2p"])
+def test_slab_upload_round_trip(lbgpu, has_gpu, transport):
     txt = case_text("mix3d")
     mono = lbgpu.Engine.from_config(txt)
-    grp = lbgpu.SlabGroup(txt, None, 3)
+    grp = lbgpu.SlabGroup(txt, None, 3, transport=transport)
     mono.init_state()
     mono.primal_step(9)
     f = mono.get_state(0)
@@ -78,3 +83,27 @@ def test_nccl_single_rank_ring_equals_monolithic(lbgpu, has_gpu, name):
     assert np.array_equal(g_m, g_r) and d_m == d_r
     assert mono.solve_primal(1e-6, 20000) == ring.solve_primal(1e-6, 20000)
     assert np.array_equal(owned(ring, 0), mono.get_state(0))
+
+
+def test_p2p_group_long_run_is_race_free(lbgpu, has_gpu):
+    """Many lock-step sweeps of four concurrently running slabs (separate
+    streams, cross-stream event waits only between neighbours) at a size where
+    the slabs' kernels overlap in time: still bitwise the monolithic run."""
+    txt = case_text("mix3d", {"lattice.nx": 64, "lattice.ny": 48, "lattice.nz": 40,
+                              "tags.design_x0": 16, "tags.design_x1": 47})
+    mono = lbgpu.Engine.from_config(txt)
+    grp = lbgpu.SlabGroup(txt, None, 4, transport="p2p")
+    mono.init_state()
+    grp.init_state()
+    assert mono.primal_step(300) == grp.step(0, 300)
+    assert np.array_equal(grp.get_state(0), mono.get_state(0))
+    assert mono.adjoint_step(150) == grp.step(1, 150)
+    assert np.array_equal(grp.get_state(1), mono.get_state(1))
+
+
+def test_p2p_link_rejects_a_non_group(lbgpu, has_gpu):
+    txt = case_text("grad2d")
+    e = lbgpu.Engine.from_config(txt)
+    import ctypes as C
+    arr = (C.c_void_p * 2)(e.h.value, e.h.value)
+    assert lbgpu.load_library().lbgpu_group_link_p2p(arr, 2) == lbgpu.E_ARG
