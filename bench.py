@@ -38,8 +38,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG_ID = "C3"
+WORKLOAD = (f"{CONFIG_ID}: mixer3d preset 256x128x128 per GPU, D3Q19+D3Q7 FMRT, "
+            "primal sweep + adjoint sweep per step")
 BYTES_PRIMAL = lambda m, s: 2 * m * s  # SURVEY.md §8(d) canonical bytes / LUP
 BYTES_ADJOINT = lambda m, s: 3 * m * s
+BYTES_PAIR = lambda m, s: 4 * m * s  # fused adjoint k + primal k+1: f read once
 
 
 def peaks() -> dict:
@@ -145,7 +148,7 @@ def run_reference(args, rank: int) -> None:
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": (tp + ta) / steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{CONFIG_ID}: mixer3d 256x128x128 D3Q19+D3Q7 FMRT", "nodes": nodes},
+        "config": {"workload": WORKLOAD, "nodes": nodes},
         "primal_mlups": nodes * steps / tp / 1e6, "adjoint_mlups": nodes * steps / ta / 1e6,
         "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": cores, "kind": "reference",
                          "sample": f"{steps} primal+adjoint sweep pairs of the full lattice, "
@@ -209,6 +212,8 @@ def main() -> None:
     eng.init_state()
     # develop a non-trivial flow before timing (the pressure wave enters)
     eng.primal_step(20, residual=False)
+    fused = eng.precision == 64  # lbgpu_pair_steps fuses adjoint k + primal k+1 at FP64
+    eng.time_pair_steps(args.warmup)
     eng.time_pairs(args.warmup)
 
     def barrier():
@@ -216,41 +221,56 @@ def main() -> None:
         if dist:
             dist.barrier()
 
+    def max_over_ranks(*vals):
+        if not dist:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return tuple(t.tolist())
+
+    # the headline: K steps of primal sweep + adjoint sweep through
+    # lbgpu_pair_steps (one fused k_pair launch per step at FP64)
     barrier()
     launches0 = eng.sweep_launches()
     with ClockSampler(local) as clk:
-        ms_tot, ms_p, ms_a = eng.time_pairs(args.steps)
+        ms_tot = eng.time_pair_steps(args.steps)
     barrier()
     launches = eng.sweep_launches() - launches0
-    if dist:
-        t = torch.tensor([ms_tot, ms_p, ms_a], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_tot, ms_p, ms_a = t.tolist()
+    (ms_tot,) = max_over_ranks(ms_tot)
+    # explanation: the two sweeps apart, CUDA events between every sweep
+    barrier()
+    _, ms_p, ms_a = eng.time_pairs(args.steps)
+    barrier()
+    # the fused sweep alone (roofline of the dominant kernel)
+    ms_k = eng.time_sweeps(2, args.steps) if fused else None
+    barrier()
+    ms_p, ms_a = max_over_ranks(ms_p, ms_a)
+    if ms_k is not None:
+        (ms_k,) = max_over_ranks(ms_k)
     # SURVEY.md §8d C3 protocol for the adjoint alone: the base frozen (the
     # steady solve_adjoint path, moment cache built once inside the timing)
     eng.time_sweeps(1, args.warmup)
     barrier()
     ms_f = eng.time_sweeps(1, args.steps)
     barrier()
-    if dist:
-        t = torch.tensor([ms_f], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_f = t.item()
+    (ms_f,) = max_over_ranks(ms_f)
     K = args.steps
     value = world * nodes * K / (ms_tot / 1e3) / 1e6
     primal_mlups = world * nodes * K / (ms_p / 1e3) / 1e6
     adjoint_mlups = world * nodes * K / (ms_a / 1e3) / 1e6
     pk = peaks()
     bp, ba = BYTES_PRIMAL(m, s), BYTES_ADJOINT(m, s)
-    ach_a = ba * nodes / (ms_a / K / 1e3) / 1e9  # per-GPU GB/s of the dominant kernel
+    bk = BYTES_PAIR(m, s)
+    ach_a = ba * nodes / (ms_a / K / 1e3) / 1e9  # per-GPU GB/s, adjoint sweep alone
     ach_p = bp * nodes / (ms_p / K / 1e3) / 1e9
+    ach_k = bk * nodes / (ms_k / K / 1e3) / 1e9 if ms_k else None
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
-        traffic = tj.get("adjoint_bytes_per_launch")
+        traffic = tj.get("pair_bytes_per_launch" if fused else "adjoint_bytes_per_launch")
 
     # e2e through the public C ABI with host buffers: each step uploads the
     # design vector (DesignField::nodes order, as a host-side optimizer such as
@@ -307,8 +327,9 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_tot / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{CONFIG_ID}: mixer3d preset 256x128x128 per GPU, D3Q19+D3Q7 "
-                               "FMRT, primal sweep + adjoint sweep per step",
+        "config": {"workload": WORKLOAD,
+                   "path": "lbgpu_pair_steps: adjoint sweep k fused with primal sweep k+1 "
+                           "(k_pair) at FP64",
                    "nodes_per_gpu": nodes,
                    "parallelism": (f"{world} x-slabs of a ({256 * world})x128x128 lattice, NCCL halo "
                                    "exchange overlapped with interior columns") if world > 1 else "1 GPU",
@@ -316,12 +337,19 @@ def main() -> None:
         "primal_mlups": primal_mlups, "adjoint_mlups": adjoint_mlups,
         "primal_hbm_gbs": ach_p, "adjoint_hbm_gbs": ach_a,
         "adjoint_frozen_base_mlups": world * nodes * K / (ms_f / 1e3) / 1e6,
-        "roofline": {"bound": "hbm", "kernel": "k_adjoint (fast, FMRT, FP64)",
-                     "achieved": ach_a, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": ach_a / pk["hbm_gbs"], "traffic": traffic,
-                     "bytes_per_lup": ba, "peak_source": pk["source"],
-                     "primal": {"achieved": ach_p, "frac": ach_p / pk["hbm_gbs"],
-                                "bytes_per_lup": bp}},
+        "roofline": ({"bound": "hbm", "kernel": "k_pair (fused adjoint k + primal k+1, FMRT, FP64)",
+                      "achieved": ach_k, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                      "frac": ach_k / pk["hbm_gbs"], "traffic": traffic,
+                      "bytes_per_lup": bk, "peak_source": pk["source"],
+                      "share_of_step": (ms_k / K) / (ms_tot / K)} if fused else
+                     {"bound": "hbm", "kernel": "k_adjoint", "achieved": ach_a,
+                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach_a / pk["hbm_gbs"],
+                      "traffic": traffic, "bytes_per_lup": ba, "peak_source": pk["source"]}),
+        "sweeps_apart": {"primal": {"mlups": primal_mlups, "achieved": ach_p,
+                                    "frac": ach_p / pk["hbm_gbs"], "bytes_per_lup": bp},
+                         "adjoint": {"mlups": adjoint_mlups, "achieved": ach_a,
+                                     "frac": ach_a / pk["hbm_gbs"], "bytes_per_lup": ba},
+                         "pair_mlups": world * nodes / ((ms_p + ms_a) / K / 1e3) / 1e6},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

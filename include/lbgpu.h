@@ -147,6 +147,14 @@ int lbgpu_get_design_values(lbgpu_engine* e, double* w_design);
 /* n x primal_step (collision.cpp:308-363); residual (nullable) = step_residual
  * of the last step (collision.cpp:365-375). */
 int lbgpu_primal_step(lbgpu_engine* e, int64_t n, double* residual);
+/* n primal+adjoint pairs, each adjoint sweep against the state its primal
+ * step just produced: one_shot_run (optimizer.cpp:25-72) at zeta = 0 without
+ * its discarded design gradient (test_optimizer.cpp:182-209), and the bench
+ * step. The product build fuses adjoint k with primal k+1 (one gather of the
+ * shared state); states equal lbgpu_primal_step(1) + lbgpu_adjoint_step(1)
+ * repeated n times, bit for bit. Residuals of the last pair (nullable). */
+int lbgpu_pair_steps(lbgpu_engine* e, int64_t n, double* primal_residual,
+                     double* adjoint_residual);
 /* tangent_solve (adjoint.cpp:422-490): forward-mode sensitivity of the
  * objective along a design direction dw (DesignField::nodes order) plus
  * d_inlet_dp, from the current primal state (frozen base). df starts at zero
@@ -248,11 +256,14 @@ int lbgpu_one_shot_range(lbgpu_engine* e, int64_t first, int64_t count, int64_t 
                          lbgpu_run_row* rows, int64_t cap, int64_t* n_rows);
 
 /* --- timing (device events on the engine stream; bench support) --- */
-/* which: 0 primal sweeps, 1 adjoint sweeps; returns elapsed milliseconds of
+/* which: 0 primal sweeps, 1 adjoint sweeps, 2 fused pair sweeps (adjoint k +
+ * primal k+1, FP64 product build); returns elapsed milliseconds of
  * `steps` back-to-back sweeps (no residual), bracketed by synchronisation.
  * Adjoint sweeps run against the frozen current primal state, with its
  * moment cache built once inside the timed region (the steady-solve path). */
 int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms);
+/* Elapsed milliseconds of lbgpu_pair_steps(n) without residuals (n >= 1). */
+int lbgpu_time_pair_steps(lbgpu_engine* e, int64_t n, double* ms);
 /* `steps` x (one primal sweep then one adjoint sweep against it), one CUDA
  * event between consecutive sweeps: total, primal-only and adjoint-only ms. */
 int lbgpu_time_pairs(lbgpu_engine* e, int64_t steps, double* ms_total, double* ms_primal,

@@ -104,6 +104,8 @@ def load_library() -> C.CDLL:
     L.lbgpu_get_design_values.argtypes = [vp, vp]
     L.lbgpu_primal_step.argtypes = [vp, i64, dp]
     L.lbgpu_primal_step_with_design.argtypes = [vp, vp, i64, dp]
+    L.lbgpu_pair_steps.argtypes = [vp, i64, dp, dp]
+    L.lbgpu_time_pair_steps.argtypes = [vp, i64, dp]
     L.lbgpu_fd_gradient.argtypes = [vp, i64, C.c_double, C.c_double, i64, i64, dp]
     L.lbgpu_tangent_solve.argtypes = [vp, vp, C.c_double, C.c_double, i64, dp, C.POINTER(i64), dp,
                                       C.POINTER(C.c_int)]
@@ -304,6 +306,22 @@ class Engine:
         self._ok(self.L.lbgpu_primal_step_with_design(self.h, _ptr(w_design), n,
                                                       C.byref(r) if residual else None))
         return r.value if residual else None
+
+    def pair_steps(self, n: int = 1, residual: bool = True):
+        """n primal+adjoint pairs (one-shot at zeta = 0 without the gradient);
+        (primal, adjoint) residuals of the last pair, or None."""
+        rp, ra = C.c_double(), C.c_double()
+        if residual:
+            self._ok(self.L.lbgpu_pair_steps(self.h, n, C.byref(rp), C.byref(ra)))
+            return rp.value, ra.value
+        self._ok(self.L.lbgpu_pair_steps(self.h, n, None, None))
+        return None
+
+    def time_pair_steps(self, n: int) -> float:
+        """Milliseconds (CUDA events) of pair_steps(n) without residuals."""
+        ms = C.c_double()
+        self._ok(self.L.lbgpu_time_pair_steps(self.h, n, C.byref(ms)))
+        return ms.value
 
     def fd_gradient(self, ordinal: int, h: float, tol: float, max_iter: int = 200000,
                     fixed_iters: int = -1) -> float:

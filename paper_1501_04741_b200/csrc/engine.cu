@@ -939,6 +939,71 @@ struct lbgpu_engine {
     }
   }
 
+  // n primal+adjoint pairs, each adjoint against the state its primal just
+  // produced: one_shot_run (optimizer.cpp:25-72) at zeta = 0 without the
+  // (then discarded) design gradient, and the bench step. The product build
+  // runs adjoint n and primal n+1 as one fused sweep (k_pair: the shared
+  // f^{n+1} gathered once, FP64); otherwise the sweeps run apart. Residuals
+  // (nullable) are those of the last pair.
+  // Fused pairs win at FP64 only (FP32 measured slower than the sweeps apart).
+  bool fuse_pairs() const { return !exact && prec == 64; }
+  void fused_pair_raw(bool resid) {
+    ++primal_steps;
+    ++adjoint_steps;
+    ++launches;
+    SweepArgs s = sweep(primal_steps, resid, nullptr);
+    void* fd = f[1 - fc];
+    void* vd = v[1 - vc];
+    const void* fsrc = f[fc];
+    const void* vsrc = v[vc];
+    auto go = [&](const SweepArgs& a) { fast::pair(a, fsrc, fd, vsrc, vd); };
+    if (xmode == 2) {
+      SweepArgs b = s;
+      b.part = 2;
+      go(b);
+      CU(cudaEventRecord(ev_bnd, st));
+      CU(cudaStreamWaitEvent(st_comm, ev_bnd, 0));
+      nccl_exchange(0, fd, st_comm);
+      nccl_exchange(1, vd, st_comm);
+      CU(cudaEventRecord(ev_halo, st_comm));
+      b.part = 1;
+      go(b);
+      CU(cudaStreamWaitEvent(st, ev_halo, 0));
+      launches += 1;
+    } else {
+      go(s);
+    }
+    fc ^= 1;
+    vc ^= 1;
+  }
+  void pair_steps(long long n, double* rp, double* ra) {
+    require_solo();
+    if (n <= 0) return;
+    const bool want = rp || ra;
+    reset_flags();
+    CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long), st));
+    if (!fuse_pairs()) {
+      for (long long k = 0; k < n; ++k) {
+        primal_launch(want && k == n - 1, nullptr);
+        adjoint_launch(0, want && k == n - 1, d_ring);
+      }
+    } else {
+      primal_launch(want && n == 1, nullptr);
+      for (long long k = 1; k < n; ++k) fused_pair_raw(want && k == n - 1);
+      adjoint_launch(0, want, d_ring);
+    }
+    CU(cudaGetLastError());
+    reduce_flags(d_flags, 1, false);
+    reduce_flags(d_ring, 1, false);
+    reduce_flags(d_flags + 1, 1, true);
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    sync();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+    if (rp) *rp = bits_to_double(h_flags[0]);
+    if (ra) *ra = bits_to_double(h_flags[4]);
+  }
+
   // solve_fixed_point / solve_adjoint stop rule (collision.cpp:377-416,
   // adjoint.cpp:256-297), batched: every step writes its residual into a ring
   // slot, the host scans once per batch, and an overshoot past the first
@@ -1936,6 +2001,40 @@ int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, in
   return guarded(e, [&] { *out = e->fd_gradient(ordinal, h, tol, max_iter, fixed_iters); });
 }
 
+int lbgpu_pair_steps(lbgpu_engine* e, int64_t n, double* primal_residual,
+                     double* adjoint_residual) {
+  if (n < 0) return LBGPU_E_ARG;
+  return guarded(e, [&] { e->pair_steps(n, primal_residual, adjoint_residual); });
+}
+
+int lbgpu_time_pair_steps(lbgpu_engine* e, int64_t n, double* ms) {
+  if (!ms || n < 1) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    e->require_solo();
+    e->reset_flags();
+    e->sync();
+    CU(cudaEventRecord(e->ev0, e->st));
+    if (!e->fuse_pairs()) {
+      for (int64_t k = 0; k < n; ++k) {
+        e->primal_launch(false, nullptr);
+        e->adjoint_launch(0, false, nullptr);
+      }
+    } else {
+      e->primal_launch(false, nullptr);
+      for (int64_t k = 1; k < n; ++k) e->fused_pair_raw(false);
+      e->adjoint_launch(0, false, nullptr);
+    }
+    CU(cudaEventRecord(e->ev1, e->st));
+    CU(cudaGetLastError());
+    CU(cudaEventSynchronize(e->ev1));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, e->ev0, e->ev1));
+    *ms = t;
+    e->reduce_flags(e->d_flags + 1, 1, true);
+    e->check_bad("iteration");
+  });
+}
+
 int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual) {
   if (kernel != 0 && kernel != 1) return LBGPU_E_ARG;
   return guarded(e, [&] {
@@ -2012,8 +2111,10 @@ int lbgpu_continue_adjoint(lbgpu_engine* e, double tol, int64_t max_iter, int64_
 }
 
 int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
-  if (!ms || steps < 0) return LBGPU_E_ARG;
+  if (!ms || steps < 0 || which < 0 || which > 2) return LBGPU_E_ARG;
   return guarded(e, [&] {
+    if (which == 2 && !e->fuse_pairs())
+      throw Fail{LBGPU_E_STATE, "fused pair sweeps run in the FP64 product build only"};
     e->reset_flags();
     e->sync();
     CU(cudaEventRecord(e->ev0, e->st));
@@ -2023,7 +2124,8 @@ int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
       lbgpu_engine::MomScope ms(e, which == 1 ? steps : 0, 0);
       for (int64_t k = 0; k < steps; ++k) {
         if (which == 0) e->primal_launch(false, nullptr);
-        else e->adjoint_launch(0, false, nullptr);
+        else if (which == 1) e->adjoint_launch(0, false, nullptr);
+        else e->fused_pair_raw(false);
       }
     }
     CU(cudaEventRecord(e->ev1, e->st));
@@ -2032,7 +2134,7 @@ int lbgpu_time_sweeps(lbgpu_engine* e, int which, int64_t steps, double* ms) {
     float t = 0.f;
     CU(cudaEventElapsedTime(&t, e->ev0, e->ev1));
     *ms = t;
-    e->check_bad(which == 0 ? "iteration" : "adjoint iteration");
+    e->check_bad(which == 1 ? "adjoint iteration" : "iteration");
   });
 }
 

@@ -193,15 +193,36 @@ __device__ __forceinline__ int code_sign(uint8_t c) { return (c & CODE_NEG) ? -1
 // drop out at compile time, and with omega_nonhydro = 1 only the shear rows
 // remain (rank 2 in 2D, 5 in 3D). BGK is A = (1 - omega) I.
 template <class L, class R, int CK>
-__device__ __forceinline__ bool fast_collide(const Model& M, PowPair pp, double omt,
-                                             const R* fin, R* out) {
-  R rho = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
+__device__ __forceinline__ bool fast_collide_m(const Model& M, PowPair pp, double omt,
+                                               const R* fin, R rho, R j0, R j1, R j2, R T,
+                                               R* out);
+// The moment sums of a gathered node, in the order fast_collide and the
+// moment-form VJP both use (so a fused sweep can share them bit for bit).
+template <class L, class R>
+__device__ __forceinline__ void node_sums(const R* fin, R& rho, R* j, R& T) {
+  R r = R(0), j0 = R(0), j1 = R(0), j2 = R(0);
   LBGPU_FOR(J, 0, L::MF, {
-    rho += fin[J];
+    r += fin[J];
     if constexpr (L::ef(J, 0) != 0) j0 = L::ef(J, 0) > 0 ? j0 + fin[J] : j0 - fin[J];
     if constexpr (L::ef(J, 1) != 0) j1 = L::ef(J, 1) > 0 ? j1 + fin[J] : j1 - fin[J];
     if constexpr (L::ef(J, 2) != 0) j2 = L::ef(J, 2) > 0 ? j2 + fin[J] : j2 - fin[J];
   });
+  R t = R(0);
+#pragma unroll
+  for (int k = 0; k < L::MT; ++k) t += fin[L::MF + k];
+  rho = r, j[0] = j0, j[1] = j1, j[2] = j2, T = t;
+}
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_collide(const Model& M, PowPair pp, double omt,
+                                             const R* fin, R* out) {
+  R rho, j[3], T;
+  node_sums<L, R>(fin, rho, j, T);
+  return fast_collide_m<L, R, CK>(M, pp, omt, fin, rho, j[0], j[1], j[2], T, out);
+}
+template <class L, class R, int CK>
+__device__ __forceinline__ bool fast_collide_m(const Model& M, PowPair pp, double omt,
+                                               const R* fin, R rho, R j0, R j1, R j2, R T_,
+                                               R* out) {
   if (!(rho > R(0))) return false;
   const R inv = R(1) / rho;
   const R u[3] = {j0 * inv, j1 * inv, j2 * inv};
@@ -237,9 +258,7 @@ __device__ __forceinline__ bool fast_collide(const Model& M, PowPair pp, double 
     });
   }
   const R* g = fin + L::MF;
-  R T = R(0);
-#pragma unroll
-  for (int j = 0; j < L::MT; ++j) T += g[j];
+  const R T = T_;
   const R om = R(omt);
   LBGPU_FOR(J, 0, L::MT, {
     const R eup = edotp<L, R, L::MF + J>(up);
@@ -1068,6 +1087,141 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
+// Fused primal + adjoint pair (product build): adjoint sweep n (base
+// f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
+// gathers it once, takes its moments once (node_sums), collides it
+// (primal_node's fast path) and runs the moment-form VJP against it
+// (adjoint_body's split path): 4 M s bytes per node for the pair instead of
+// 5 M s. Each half is bitwise the stand-alone sweep (same functions, same
+// operands). Side-list nodes' adjoint half goes to k_adjoint_side as usual.
+template <class L, class R, int CK, bool RESID>
+__device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__ fsrc,
+                                          R* __restrict__ fdst, const R* __restrict__ vsrc,
+                                          R* __restrict__ vdst, int x, int y, int z,
+                                          unsigned long long& rP, unsigned long long& rA) {
+  using namespace detail;
+  const Geom& g = a.g;
+  const long long N = g.N;
+  const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
+  const uint8_t code = a.t.code[idx];
+  const int tag = code & TAG_MASK;
+  const bool face = is_face(tag);
+  const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
+  const Nbr nb = make_nbr(g, x, y, z);
+  constexpr bool kStage = LBGPU_ADJ_STAGE && sizeof(R) == 8;
+  __shared__ R vsm[kStage ? L::M * 128 : 1];
+  R* my = vsm + (kStage ? threadIdx.x : 0);
+  if constexpr (kStage)
+    if (!side) gather_async<L, R, +1>(vsrc, N, nb, my, 128);
+  R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
+  FaceState<R> fs{};
+  bool okP = true, okA = true;
+  {
+    R f[L::M], out[L::M];
+    gather<L, R, -1>(fsrc, N, nb, f);
+    double w = 1.0;
+    PowPair pp{};
+    double omt = 0.0;
+    if (tag == TAG_WALL) {
+      LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
+    } else if (tag == TAG_HEATER) {
+      LBGPU_FOR(P, 0, L::MF, { out[P] = f[L::oppf(P)]; });
+      const R Th = R(a.t.bcT[idx]);
+#pragma unroll
+      for (int j = 0; j < L::MT; ++j) out[L::MF + j] = R(L::wt(j)) * Th * (R(1) + R(3) * R(0));
+    } else {
+      w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+      pp = node_pp<false>(a.M, a.t, idx, code, w);
+      omt = node_omt<R>(a.M, a.t, code, w);
+      if (face) {
+        const bool inlet = tag == TAG_INLET;
+        const double bcT = a.t.bcT[idx];
+        face_dispatch<L>(code, [&]<int AX, int SG>() {
+          fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, f);
+        });
+      }
+    }
+    node_sums<L, R>(f, rho, jv, T);
+    if (!(tag == TAG_WALL || tag == TAG_HEATER))
+      okP = fast_collide_m<L, R, CK>(a.M, pp, omt, f, rho, jv[0], jv[1], jv[2], T, out);
+    store_node<L, R, RESID>(fsrc, fdst, N, idx, f, out, rP, !face);
+    push_halo<L, R, -1>(a, x, y, z, out);
+  }
+  if (!side) {
+    R vin[L::M], vout[L::M];
+    if constexpr (kStage) {
+      cp_async_wait_all();
+      LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
+    } else {
+      gather<L, R, +1>(vsrc, N, nb, vin);
+    }
+    if (tag == TAG_WALL) {
+      LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+    } else if (tag == TAG_HEATER) {
+      LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+#pragma unroll
+      for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
+    } else {
+      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+      const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
+      const double omt = node_omt<R>(a.M, a.t, code, w);
+      okA = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout, vout + L::MF);
+      if (face) {
+        const bool inlet = tag == TAG_INLET;
+        face_dispatch<L>(code, [&]<int AX, int SG>() {
+          face_reverse<L, R, AX, SG>(inlet, fs, vout);
+        });
+      }
+    }
+    if (a.M.obj_on && (code & CODE_SUPPORT)) okA = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && okA;
+    store_node<L, R, RESID>(vsrc, vdst, N, idx, vin, vout, rA);
+    push_halo<L, R, +1>(a, x, y, z, vout);
+  }
+  if (!(okP && okA)) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+}
+
+// FP32 pairs measured C3 (MLUPS): 4 blocks 9,968, 5: 10,188, 6: 9,903, 8
+// (216 B spill) 8,321 -- all below the two FP32 sweeps run apart (10,433), so
+// the engine fuses FP64 pairs only (7,067 against 6,109 apart).
+#ifndef LBGPU_PAIR_MINB32
+#define LBGPU_PAIR_MINB32 5
+#endif
+#define LBGPU_PAIR_BOUNDS(R) \
+  __launch_bounds__(128, sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_ADJ_MINB)
+template <class L, class R, int CK, bool RESID>
+__global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
+                                                        R* __restrict__ fdst,
+                                                        const R* __restrict__ vsrc,
+                                                        R* __restrict__ vdst) {
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long rP = 0, rA = 0;
+  if (x < a.g.x1)
+    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, x, blockIdx.y, a.g.z0 + blockIdx.z, rP, rA);
+  if constexpr (RESID) {
+    detail::block_max_bits(rP, a.fl.resid);
+    detail::block_max_bits(rA, a.fl.aux);
+  }
+}
+
+template <class L, class R, int CK, bool RESID>
+__global__ void LBGPU_PAIR_BOUNDS(R) k_pair_cols(Launch a, const R* __restrict__ fsrc,
+                                                             R* __restrict__ fdst,
+                                                             const R* __restrict__ vsrc,
+                                                             R* __restrict__ vdst, int c0, int c1) {
+  const long long yz = (long long)a.g.ny * a.g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned long long rP = 0, rA = 0;
+  if (t < 2 * yz) {
+    const long long r = t % yz;
+    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, t < yz ? c0 : c1, int(r % a.g.ny),
+                               int(r / a.g.ny), rP, rA);
+  }
+  if constexpr (RESID) {
+    detail::block_max_bits(rP, a.fl.resid);
+    detail::block_max_bits(rA, a.fl.aux);
+  }
+}
+
 // Per-design-node gradient (param_gradient's design part, adjoint.cpp:377-398)
 // with, when UPDATE, the one-shot composite/ascent step fused in
 // (optimizer.cpp:41-45, descent_update :8-16). The node list holds local
@@ -1450,6 +1604,44 @@ void primal(const SweepArgs& s, const void* src, void* dst) {
 #if defined(LBGPU_PART_ADJOINT)
 void adjoint(const SweepArgs& s, const void* base, const void* src, void* dst) {
   LBGPU_LR_DISPATCH(s.dim, s.prec, (adjoint_l<L, R, 0>(s, base, src, dst)));
+}
+// k_pair over s.part's columns, then the side-list adjoint nodes (part != 1);
+// the primal residual goes to a.fl.resid, the adjoint's to a.fl.aux.
+template <class L, class R, int CK, bool RES>
+void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, void* vd_) {
+  const R* fsrc = static_cast<const R*>(fs_);
+  const R* vsrc = static_cast<const R*>(vs_);
+  R* fdst = static_cast<R*>(fd_);
+  R* vdst = static_cast<R*>(vd_);
+  Launch a = s.a;
+  if (s.part == 2) {
+    const long long n = 2ll * a.g.ny * a.g.nz;
+    k_pair_cols<L, R, CK, RES><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
+        a, fsrc, fdst, vsrc, vdst, a.g.x0, a.g.x1 - 1);
+  } else {
+    if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+    if (a.g.x1 > a.g.x0) {
+      const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+      dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+      k_pair<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
+    }
+  }
+  if (s.n_adj_side > 0 && s.part != 1) {
+    Launch as = s.a;
+    as.fl.resid = s.a.fl.aux;  // the side nodes' residual is the adjoint's
+    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
+        as, fsrc, vsrc, vdst, s.adj_side, s.n_adj_side);
+  }
+}
+void pair(const SweepArgs& s, const void* fsrc, void* fdst, const void* vsrc, void* vdst) {
+#if LBGPU_EXACT
+  (void)s, (void)fsrc, (void)fdst, (void)vsrc, (void)vdst;  // the exact build runs the sweeps apart
+#else
+  LBGPU_LR_DISPATCH(s.dim, s.prec, {
+    if (s.resid) LBGPU_CK_DISPATCH((pair_t<L, R, CKV, true>(s, fsrc, fdst, vsrc, vdst)));
+    else LBGPU_CK_DISPATCH((pair_t<L, R, CKV, false>(s, fsrc, fdst, vsrc, vdst)));
+  });
+#endif
 }
 void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom) {
   const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);

@@ -81,6 +81,7 @@ struct SweepArgs {
               void* out, cudaStream_t st);                                                 \
   void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
   void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom);         \
+  void pair(const SweepArgs& s, const void* fsrc, void* fdst, const void* vsrc, void* vdst);  \
   void tangent(const SweepArgs& s, const void* base, const void* src, void* dst,              \
                const double* dw, double d_rho_in);                                           \
   void tangent_terms(const Launch& a, int dim, int prec, const void* base, const void* df,   \

@@ -313,3 +313,30 @@ def test_frozen_base_moment_cache_is_bitwise(lbgpu, has_gpu, name):
     assert ra == rb
     assert np.array_equal(a.get_state(1), b.get_state(1))
     assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("exact", [False, True])
+def test_pair_steps_equal_separate_sweeps(lbgpu, has_gpu, name, exact):
+    """lbgpu_pair_steps (product build: adjoint k fused with primal k+1 in one
+    sweep, k_pair) is bitwise n x (primal_step(1) + adjoint_step(1)): states,
+    residuals of the last pair, and the gradient afterwards."""
+    txt = case_text(name)
+    a = lbgpu.Engine.from_config(txt, exact=exact)
+    b = lbgpu.Engine.from_config(txt, exact=exact)
+    for e in (a, b):
+        e.init_state()
+        e.primal_step(25)
+    for n in (1, 2, 7):
+        rp, ra = a.pair_steps(n)
+        for _ in range(n):
+            rpb = b.primal_step(1)
+            rab = b.adjoint_step(1)
+        assert (rp, ra) == (rpb, rab)
+        assert np.array_equal(a.get_state(0), b.get_state(0))
+        assert np.array_equal(a.get_state(1), b.get_state(1))
+    assert a.pair_steps(3, residual=False) is None
+    for _ in range(3):
+        b.primal_step(1), b.adjoint_step(1)
+    assert np.array_equal(a.get_state(1), b.get_state(1))
+    assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])

@@ -83,6 +83,11 @@ def test_nccl_single_rank_ring_equals_monolithic(lbgpu, has_gpu, name):
     assert np.array_equal(g_m, g_r) and d_m == d_r
     assert mono.solve_primal(1e-6, 20000) == ring.solve_primal(1e-6, 20000)
     assert np.array_equal(owned(ring, 0), mono.get_state(0))
+    # fused pairs: both fields' halos after every k_pair (boundary columns
+    # first, interior overlapped with the two exchanges)
+    assert mono.pair_steps(6) == ring.pair_steps(6)
+    assert np.array_equal(owned(ring, 0), mono.get_state(0))
+    assert np.array_equal(owned(ring, 1), mono.get_state(1))
 
 
 def test_p2p_group_long_run_is_race_free(lbgpu, has_gpu):

@@ -45,17 +45,23 @@ def launches(path):
 
 
 def full(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
+    """rep: a .ncu-rep, or the CSV of `ncu -i rep --page raw --csv`; several
+    may be joined with commas (each parsed with its own header)."""
     res = []
-    for r in rows[2:]:
-        d = {"kernel": r[hdr.index("Kernel Name")]}
-        for m in METRICS:
-            if m in hdr:
-                d[m] = f"{r[hdr.index(m)]} {units[hdr.index(m)]}".strip()
-        res.append(d)
+    for part in rep.split(","):
+        if part.endswith(".csv"):
+            raw = open(part).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", part, "--page", "raw", "--csv"],
+                                 capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, units = rows[0], rows[1]
+        for r in rows[2:]:
+            d = {"kernel": r[hdr.index("Kernel Name")]}
+            for m in METRICS:
+                if m in hdr:
+                    d[m] = f"{r[hdr.index(m)]} {units[hdr.index(m)]}".strip()
+            res.append(d)
     return res
 
 
@@ -69,7 +75,9 @@ def main():
                  " (C3, FP64). Times are cold-cache and serialised: compare shares.\n\n")
         fh.write(table + "\n")
     with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as fh:
-        fh.write(f"# {tag}: ncu --set full (C3 256x128x128, FP64)\n\n")
+        fh.write(f"# {tag}: ncu --set full (C3 256x128x128, FP64)\n\n"
+                 "One launch per kernel from `bench.py --steps 20 --warmup 3 --no-cpu-baseline "
+                 "--e2e-steps 2` (-s 5 -c 1 each), --clock-control none, cold cache.\n\n")
         for d in kern:
             fh.write(f"## {d['kernel']}\n\n")
             for m in METRICS:
@@ -83,7 +91,8 @@ def main():
             v, u = d[m].split(" ")[0].replace(",", ""), d[m].split(" ")[1] if " " in d[m] else ""
             return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-        key = "adjoint_bytes_per_launch" if "k_adjoint" in d["kernel"] else "primal_bytes_per_launch"
+        key = ("pair_bytes_per_launch" if "k_pair" in d["kernel"] else
+               "adjoint_bytes_per_launch" if "k_adjoint" in d["kernel"] else "primal_bytes_per_launch")
         tj[key] = b
     tj["source"] = f"profiles/{tag}_ncu_full.md (ncu --set full, C3 FP64)"
     with open(os.path.join(PROF, "traffic.json"), "w") as fh:

@@ -24,7 +24,12 @@ for prec in precs:
     t0 = time.perf_counter()
     e.adjoint_step(K, residual=False)
     tf = (time.perf_counter() - t0) * 1e3
+    e.time_pair_steps(5)
+    tpair = e.time_pair_steps(K)
     print(json.dumps({"lib": os.environ.get("LBGPU_LIB", "default"), "prec": prec,
+                      "pair_mlups_separate": round(e.n * K / t / 1e3, 1),
+                      "pair_mlups_fused": round(e.n * K / tpair / 1e3, 1),
+                      "fused_pair_gbs": round(4 * e.m * s * e.n * K / tpair / 1e6, 1),
                       "primal_gbs": round(2 * e.m * s * e.n * K / tp / 1e6, 1),
                       "adjoint_gbs": round(3 * e.m * s * e.n * K / ta / 1e6, 1),
                       "adjoint_mlups": round(e.n * K / ta / 1e3, 1),
