@@ -1087,6 +1087,15 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
+// Experiment knob: stage the f gather through shared memory as well (then
+// 64-thread blocks keep the static shared memory under 48 KB). Measured C3
+// FP64: 5,472 MLUPS per pair against 7,067 with it off.
+#ifndef LBGPU_PAIR_STAGE2
+#define LBGPU_PAIR_STAGE2 0
+#endif
+template <class R>
+constexpr int kPairThreads = (LBGPU_PAIR_STAGE2 && sizeof(R) == 8) ? 64 : 128;
+
 // Fused primal + adjoint pair (product build): adjoint sweep n (base
 // f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
 // gathers it once, takes its moments once (node_sums), collides it
@@ -1109,16 +1118,27 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
   const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
   const Nbr nb = make_nbr(g, x, y, z);
   constexpr bool kStage = LBGPU_ADJ_STAGE && sizeof(R) == 8;
-  __shared__ R vsm[kStage ? L::M * 128 : 1];
+  constexpr bool kStage2 = LBGPU_PAIR_STAGE2 && sizeof(R) == 8;  // f staged too
+  constexpr int kTB = kPairThreads<R>;
+  __shared__ R fsm[kStage2 ? L::M * kTB : 1];
+  __shared__ R vsm[kStage ? L::M * kTB : 1];
+  R* myf = fsm + (kStage2 ? threadIdx.x : 0);
   R* my = vsm + (kStage ? threadIdx.x : 0);
+  if constexpr (kStage2) gather_async<L, R, -1>(fsrc, N, nb, myf, kTB);
   if constexpr (kStage)
-    if (!side) gather_async<L, R, +1>(vsrc, N, nb, my, 128);
+    if (!side) gather_async<L, R, +1>(vsrc, N, nb, my, kTB);
   R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
   FaceState<R> fs{};
   bool okP = true, okA = true;
   {
     R f[L::M], out[L::M];
-    gather<L, R, -1>(fsrc, N, nb, f);
+    if constexpr (kStage2) {
+      if (!side) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else cp_async_wait_all();
+      LBGPU_FOR(P, 0, L::M, { f[P] = myf[P * kTB]; });
+    } else {
+      gather<L, R, -1>(fsrc, N, nb, f);
+    }
     double w = 1.0;
     PowPair pp{};
     double omt = 0.0;
@@ -1151,7 +1171,7 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
     R vin[L::M], vout[L::M];
     if constexpr (kStage) {
       cp_async_wait_all();
-      LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
+      LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * kTB]; });
     } else {
       gather<L, R, +1>(vsrc, N, nb, vin);
     }
@@ -1186,8 +1206,9 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
 #ifndef LBGPU_PAIR_MINB32
 #define LBGPU_PAIR_MINB32 5
 #endif
-#define LBGPU_PAIR_BOUNDS(R) \
-  __launch_bounds__(128, sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_ADJ_MINB)
+#define LBGPU_PAIR_BOUNDS(R)                                                   \
+  __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_ADJ_MINB) * \
+                                         (128 / kPairThreads<R>))
 template <class L, class R, int CK, bool RESID>
 __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
                                                         R* __restrict__ fdst,
@@ -1614,14 +1635,15 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
   R* fdst = static_cast<R*>(fd_);
   R* vdst = static_cast<R*>(vd_);
   Launch a = s.a;
+  constexpr int TB = kPairThreads<R>;
   if (s.part == 2) {
     const long long n = 2ll * a.g.ny * a.g.nz;
-    k_pair_cols<L, R, CK, RES><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
+    k_pair_cols<L, R, CK, RES><<<unsigned((n + TB - 1) / TB), TB, 0, a.stream>>>(
         a, fsrc, fdst, vsrc, vdst, a.g.x0, a.g.x1 - 1);
   } else {
     if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
     if (a.g.x1 > a.g.x0) {
-      const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+      const int bx = (a.g.x1 - a.g.x0) >= TB ? TB : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
       dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
       k_pair<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
     }
