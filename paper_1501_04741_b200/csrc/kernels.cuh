@@ -1206,8 +1206,13 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
 #ifndef LBGPU_PAIR_MINB32
 #define LBGPU_PAIR_MINB32 5
 #endif
+// FP64 pair, C3 MLUPS: 3 blocks (168 regs) 6,711; 4 (128 regs) 7,067; 5 (96
+// regs + 248 B spill) 5,381.
+#ifndef LBGPU_PAIR_MINB
+#define LBGPU_PAIR_MINB LBGPU_ADJ_MINB
+#endif
 #define LBGPU_PAIR_BOUNDS(R)                                                   \
-  __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_ADJ_MINB) * \
+  __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_PAIR_MINB) * \
                                          (128 / kPairThreads<R>))
 template <class L, class R, int CK, bool RESID>
 __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
