@@ -46,9 +46,14 @@ def sweeps(e, K=50):
     s = 8 if e.precision == 64 else 4
     sl = e.slab()
     n = e.n // sl["nxl"] * sl["span"]
-    return {"primal_mlups": n * K / tp / 1e3, "adjoint_mlups": n * K / ta / 1e3,
-            "primal_gbs": 2 * e.m * s * n * K / tp / 1e6,
-            "adjoint_gbs": 3 * e.m * s * n * K / ta / 1e6}
+    out = {"primal_mlups": n * K / tp / 1e3, "adjoint_mlups": n * K / ta / 1e3,
+           "primal_gbs": 2 * e.m * s * n * K / tp / 1e6,
+           "adjoint_gbs": 3 * e.m * s * n * K / ta / 1e6}
+    e.time_pair_steps(3)
+    out["pair_mlups"] = n * K / e.time_pair_steps(K) / 1e3  # lbgpu_pair_steps (fused at FP64)
+    e.time_sweeps(1, 3)
+    out["adjoint_frozen_base_mlups"] = n * K / e.time_sweeps(1, K) / 1e3
+    return out
 
 
 if want("C1"):
@@ -160,11 +165,12 @@ if want("C2"):
 
 if want("C3"):
     res = {}
-    for prec in (64, 32):
-        e = P.Engine.from_config(config_text("C3"), {"model.precision": prec})
+    for name, ov in (("fp64", {}), ("fp32", {"model.precision": 32}),
+                     ("bgk_fp64", {"model.collision": "bgk"})):
+        e = P.Engine.from_config(config_text("C3"), ov)
         e.init_state()
         e.primal_step(20, residual=False)
-        res[f"fp{prec}"] = sweeps(e)
+        res[name] = sweeps(e)
         e.close()
     out["C3"] = res
     print("C3", json.dumps(res), flush=True)
@@ -183,7 +189,43 @@ if want("C4"):
     r_.init_state()
     tp = r_.time_steps(0, CORES, 1)
     ta = r_.time_steps(1, CORES, 1)
-    out["C4"] = {"nodes": e.n, "one_shot_iterations_per_s": K / dt,
+    # parity: the C2 warm-start protocol at 128x32x32 (C4
+    # proportions), 20 one-shot iterations from the same (f, v, w) on both
+    # engines; then 3 full-size iterations from a GPU-warmed state.
+    def warm_parity(txt_warm, txt_run, warm, iters):
+        g = P.Engine.from_config(txt_warm)
+        g.init_state()
+        g.one_shot(np.zeros(warm), np.zeros(warm), record_interval=warm)
+        f0, v0, w0 = g.get_state(0), g.get_state(1), g.design()
+        rows = g.one_shot(np.full(iters, 1e-4), np.zeros(iters), record_interval=1)
+        wg = g.design()
+        g.close()
+        rr = O.RefOracle(txt_run)
+        rr.set_state(0, f0)
+        rr.set_state(1, v0)
+        rr.set_design(w0)
+        t0 = time.perf_counter()
+        rrows = rr.one_shot(iters, 1)
+        ref_s = time.perf_counter() - t0
+        return {"warm_iterations": warm, "iterations": iters,
+                "objective_trace_gpu": rows[:, 2].tolist(),
+                "objective_trace_reference": rrows[:, 2].tolist(),
+                "max_abs_w_diff": float(np.max(np.abs(wg - rr.tables()["w"]))),
+                "max_rel_objective_diff": float(np.max(np.abs(rows[:, 2] - rrows[:, 2]) /
+                                                       np.abs(rrows[:, 2]))),
+                "max_rel_gradnorm_diff": float(np.max(np.abs(rows[:, 6] - rrows[:, 6]) /
+                                                      np.abs(rrows[:, 6]))),
+                "design_moved": float(np.max(np.abs(wg - w0))),
+                "reference_seconds_1thread": ref_s}
+    small = {"lattice.nx": 128, "lattice.ny": 32, "lattice.nz": 32, "tags.design_x0": 37,
+             "tags.design_x1": 91, "tags.heater_x0": 55, "tags.heater_x1": 72}
+    par_small = warm_parity(config_text("C4", {**small, "optimizer.zeta_stages": "0:0"}),
+                            config_text("C4", {**small, "optimizer.zeta_stages": "0:0.0001"}),
+                            4000, 20)
+    par_full = warm_parity(config_text("C4", {"optimizer.zeta_stages": "0:0"}),
+                           config_text("C4", {"optimizer.zeta_stages": "0:0.0001"}), 4000, 3)
+    out["C4"] = {"parity_128x32x32": par_small, "parity_full_size": par_full,
+                 "nodes": e.n, "one_shot_iterations_per_s": K / dt,
                  "one_shot_node_iterations_mlups": e.n * K / dt / 1e6, **sw,
                  "reference_primal_plus_adjoint_seconds_per_iteration": tp + ta,
                  "reference_cores": CORES}
