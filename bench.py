@@ -136,7 +136,8 @@ def run_reference(args, rank: int) -> None:
     r = O.RefOracle(txt)
     nodes = r.n
     r.init_state()
-    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))
+    # bounded CPU sample: <= 3 warm-up and <= 3 timed pairs (~0.8 s each at C3)
+    warm, steps = min(max(args.warmup, 3), 3), max(1, min(args.steps, 3))
     for _ in range(warm):
         r.time_steps(0, cores, 1)
         r.time_steps(1, cores, 1)
