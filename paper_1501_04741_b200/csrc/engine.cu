@@ -1009,6 +1009,55 @@ struct lbgpu_engine {
   // slot, the host scans once per batch, and an overshoot past the first
   // r <= tol is undone from a snapshot and replayed, so the stop iteration
   // and final state are exactly the per-step loop's.
+  // Small lattices are launch-bound (C1: ~5.5 us per step, of which the sweep
+  // is ~1 us): full ring batches of the tol-stop solver run as a captured CUDA
+  // graph of kRing sweeps (their residual slots baked in, step keys relative
+  // to the batch), one graph per starting buffer parity, per solve.
+  static constexpr long long kGraphMaxNodes = 1ll << 20;
+  struct RingGraphs {
+    cudaGraphExec_t ex[2] = {nullptr, nullptr};
+    ~RingGraphs() {
+      for (auto& g : ex)
+        if (g) cudaGraphExecDestroy(g);
+    }
+  };
+  void capture_ring(int which, int kernel, int par, cudaGraphExec_t* out) {
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int k = 0; k < kRing; ++k) {
+        const int p = (par + k) & 1;
+        SweepArgs s = sweep((unsigned long long)(k + 1), true, d_ring + k);
+        if (which == 0) {
+          if (exact) exact::primal(s, f[p], f[1 - p]);
+          else fast::primal(s, f[p], f[1 - p]);
+        } else if (which == 1) {
+          if (kernel == 0 && mom_base && mom_base == f[fc]) s.mom = d_mom;
+          if (kernel) {
+            if (exact) exact::adjoint_dual(s, f[fc], v[p], v[1 - p]);
+            else fast::adjoint_dual(s, f[fc], v[p], v[1 - p]);
+          } else {
+            if (exact) exact::adjoint(s, f[fc], v[p], v[1 - p]);
+            else fast::adjoint(s, f[fc], v[p], v[1 - p]);
+          }
+        } else {
+          if (exact) exact::tangent(s, f[fc], tg[p], tg[1 - p], d_dw, tangent_drho);
+          else fast::tangent(s, f[fc], tg[p], tg[1 - p], d_dw, tangent_drho);
+        }
+      }
+      CU(cudaGetLastError());
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      (void)cudaGetLastError();
+      throw;
+    }
+    CU(cudaStreamEndCapture(st, &g));
+    const cudaError_t r = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    CU(r);
+  }
+
   void solve(int which, double tol, long long max_iter, long long fixed, int kernel,
              long long* iters, double* resid, int* conv, bool reset_v = true) {
     require_solo();
@@ -1024,6 +1073,8 @@ struct lbgpu_engine {
     long long it = 0;
     double r = 0.0;
     long long batch = 1;
+    const bool graphs = xmode == 0 && N <= kGraphMaxNodes;
+    RingGraphs rg;
     while (it < n) {
       const long long b = std::min<long long>({batch, n - it, (long long)kRing});
       void** buf = which == 0 ? f : which == 1 ? v : tg;
@@ -1033,10 +1084,18 @@ struct lbgpu_engine {
       const long long steps0 = steps;
       if (fixed < 0 && b > 1) CU(cudaMemcpyAsync(snap, buf[cur], field_bytes(), cudaMemcpyDeviceToDevice, st));
       CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long) * b, st));
-      for (long long k = 0; k < b; ++k) {
-        if (which == 0) primal_launch(true, d_ring + k);
-        else if (which == 1) adjoint_launch(kernel, true, d_ring + k);
-        else tangent_launch(true, d_ring + k);
+      const bool rel = graphs && b == kRing;  // graph batch: step keys 1..kRing
+      if (rel) {
+        if (!rg.ex[cur]) capture_ring(which, kernel, cur, &rg.ex[cur]);
+        CU(cudaGraphLaunch(rg.ex[cur], st));
+        steps += kRing;  // kRing is even: the buffer parity is back where it started
+        launches += kRing;
+      } else {
+        for (long long k = 0; k < b; ++k) {
+          if (which == 0) primal_launch(true, d_ring + k);
+          else if (which == 1) adjoint_launch(kernel, true, d_ring + k);
+          else tangent_launch(true, d_ring + k);
+        }
       }
       CU(cudaGetLastError());
       reduce_flags(d_ring, size_t(b), false);
@@ -1049,8 +1108,10 @@ struct lbgpu_engine {
       for (long long k = 0; k < b; ++k) {
         const double rk = bits_to_double(h_flags[4 + k]);
         const long long itk = it + k + 1;
-        const bool badk = h_flags[1] != kNoBad && (long long)(h_flags[1] >> 40) == steps0 + k + 1;
-        if (badk) raise_bad(h_flags[1], what);
+        const long long key_step = rel ? k + 1 : steps0 + k + 1;
+        const bool badk = h_flags[1] != kNoBad && (long long)(h_flags[1] >> 40) == key_step;
+        if (badk)
+          raise_bad(rel ? h_flags[1] + ((unsigned long long)steps0 << 40) : h_flags[1], what);
         if (!std::isfinite(rk)) {
           reset_flags();
           if (which == 2)  // adjoint.cpp:472-473
