@@ -179,6 +179,15 @@ int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, in
  * call returns. residual (nullable) as lbgpu_primal_step. */
 int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64_t n,
                                   double* residual);
+/* One one_shot_run iteration head (optimizer.cpp:33-34: primal_step, then
+ * adjoint_step against the new f) behind the design write-back of
+ * optimizer.cpp:200-202, plus J = evaluate_raw of the new state
+ * (objective.cpp:64-72). Equals lbgpu_primal_step_with_design(1) +
+ * lbgpu_adjoint_step(1, kernel 0) + lbgpu_objective bit for bit; the design
+ * upload, the primal z-chunks and the adjoint z-chunks run as one overlapped
+ * pipeline (3D, product build). Residuals and objective are nullable. */
+int lbgpu_pair_step_with_design(lbgpu_engine* e, const double* w_design, double* primal_residual,
+                                double* adjoint_residual, double* objective);
 /* n x adjoint_step (adjoint.cpp:206-254) against the current primal state.
  * kernel: 0 analytic, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18). */
 int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual);

@@ -105,6 +105,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_primal_step.argtypes = [vp, i64, dp]
     L.lbgpu_primal_step_with_design.argtypes = [vp, vp, i64, dp]
     L.lbgpu_pair_steps.argtypes = [vp, i64, dp, dp]
+    L.lbgpu_pair_step_with_design.argtypes = [vp, vp, dp, dp, dp]
     L.lbgpu_time_pair_steps.argtypes = [vp, i64, dp]
     L.lbgpu_fd_gradient.argtypes = [vp, i64, C.c_double, C.c_double, i64, i64, dp]
     L.lbgpu_tangent_solve.argtypes = [vp, vp, C.c_double, C.c_double, i64, dp, C.POINTER(i64), dp,
@@ -306,6 +307,21 @@ class Engine:
         self._ok(self.L.lbgpu_primal_step_with_design(self.h, _ptr(w_design), n,
                                                       C.byref(r) if residual else None))
         return r.value if residual else None
+
+    def pair_step_with_design(self, w_design: np.ndarray, residual: bool = True,
+                              objective: bool = True):
+        """New design values, one primal step, one adjoint step against the new
+        state and J of that state (optimizer.cpp:33-34, :200-202), as one
+        overlapped pipeline. Returns (primal_residual, adjoint_residual, J),
+        None where not requested."""
+        w_design = np.ascontiguousarray(w_design, np.float64)
+        assert w_design.size == self.n_design
+        rp, ra, j = C.c_double(), C.c_double(), C.c_double()
+        self._ok(self.L.lbgpu_pair_step_with_design(
+            self.h, _ptr(w_design), C.byref(rp) if residual else None,
+            C.byref(ra) if residual else None, C.byref(j) if objective else None))
+        return (rp.value if residual else None, ra.value if residual else None,
+                j.value if objective else None)
 
     def pair_steps(self, n: int = 1, residual: bool = True):
         """n primal+adjoint pairs (one-shot at zeta = 0 without the gradient);

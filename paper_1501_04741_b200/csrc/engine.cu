@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -297,6 +299,8 @@ struct lbgpu_engine {
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   cudaStream_t st_h2d = nullptr;        // design uploads pipelined under the first sweep
   std::vector<cudaEvent_t> ev_chunk;    // one per z-chunk of that upload (+1: start)
+  cudaStream_t st_adj = nullptr;        // design pair: adjoint z-chunks behind the primal's
+  std::vector<cudaEvent_t> ev_prim;     // one per primal z-chunk (+1: adjoint done)
   bool owns_stream = true;
   long long N = 0;
   int device = 0;
@@ -354,6 +358,8 @@ struct lbgpu_engine {
     if (st_comm) cudaStreamDestroy(st_comm);
     for (cudaEvent_t ev : ev_chunk) cudaEventDestroy(ev);
     if (st_h2d) cudaStreamDestroy(st_h2d);
+    for (cudaEvent_t ev : ev_prim) cudaEventDestroy(ev);
+    if (st_adj) cudaStreamDestroy(st_adj);
     for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {f[0], f[1], v[0], v[1], snap, tg[0], tg[1]}) cudaFree(p);
@@ -856,6 +862,166 @@ struct lbgpu_engine {
     return want_resid ? bits_to_double(h_flags[0]) : 0.0;
   }
 
+  // Queue the z-chunked H2D copy of design values (after everything already
+  // on st): chunk c covers design positions [ib[c], ib[c+1]) = z planes
+  // [zb[c], zb[c+1]); ev_chunk[c] fires when its slice has landed.
+  void design_bounds(long long* ib, int* zb) const {
+    const long long plane = (long long)nx * ny;
+    for (int c = 0; c <= kChunks; ++c) {
+      zb[c] = int((long long)nz * c / kChunks);
+      ib[c] = std::lower_bound(design.begin(), design.end(), plane * zb[c]) - design.begin();
+    }
+  }
+  void ensure_h2d() {
+    if (!d_wvals) CU(cudaMalloc(&d_wvals, sizeof(double) * std::max<size_t>(design.size(), 1)));
+    if (!st_h2d) {
+      CU(cudaStreamCreateWithFlags(&st_h2d, cudaStreamNonBlocking));
+      ev_chunk.resize(kChunks + 1);
+      for (cudaEvent_t& ev : ev_chunk) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+  }
+  void queue_design_upload(const double* wd, long long* ib, int* zb, bool mark = true) {
+    ensure_h2d();
+    // the staging buffer is free once everything queued before us has run
+    // (mark = false: the caller recorded ev_chunk[kChunks] on st already)
+    if (mark) CU(cudaEventRecord(ev_chunk[kChunks], st));
+    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
+    design_bounds(ib, zb);
+    for (int c = 0; c < kChunks; ++c)
+      if (ib[c + 1] > ib[c]) {
+        CU(cudaMemcpyAsync(d_wvals + ib[c], wd + ib[c], sizeof(double) * (ib[c + 1] - ib[c]),
+                           cudaMemcpyHostToDevice, st_h2d));
+        CU(cudaEventRecord(ev_chunk[c], st_h2d));
+      }
+  }
+  bool design_chunking() const {
+    return !design.empty() && !exact && dim == 3 && xmode != 2 && nz >= 2 * kChunks;
+  }
+
+  // One iteration head of one_shot_run (optimizer.cpp:33-34: primal_step,
+  // then adjoint_step against the new f) behind a design write-back
+  // (optimizer.cpp:200-202), with J = evaluate_raw of the new state
+  // (objective.cpp:64-72). Same results as primal_step_with_design(1) +
+  // adjoint_step(1) + objective, bit for bit. Three overlapped pipelines:
+  // the H2D copy of the design in z-chunks; the primal sweep chunk c after
+  // its design slice; the adjoint sweep chunk c on a second stream after
+  // primal chunk c+1 (it gathers the new f from planes z-1..z+1; chunks 0
+  // and kChunks-1 also need the periodic z neighbour, so they go last).
+  // C3 (LBGPU_TRACE_PAIR timeline): the 16 MB upload lands at 0.34 ms, the
+  // step ends at 0.90 ms against 0.91 for the three calls; the adjoint,
+  // HBM-bound, cannot start before primal chunk 2. Sweeping the design-free
+  // columns first (primal, then adjoint, on a low-priority stream, the
+  // design chunks on a high-priority one) measured 0.99-1.10 ms: the narrow
+  // column launches run at 60% of the full sweep's rate.
+  // LBGPU_TRACE_PAIR=1: print each pipeline stage's finish time (development).
+  std::vector<cudaEvent_t> trace_ev;
+  std::vector<std::string> trace_name;
+  void trace(const char* what, cudaStream_t s_) {
+    static const bool on = std::getenv("LBGPU_TRACE_PAIR") != nullptr;
+    if (!on) return;
+    if (trace_ev.size() <= trace_name.size()) {
+      trace_ev.emplace_back();
+      CU(cudaEventCreate(&trace_ev.back()));
+    }
+    CU(cudaEventRecord(trace_ev[trace_name.size()], s_));
+    trace_name.emplace_back(what);
+  }
+  void trace_print() {
+    if (trace_name.empty()) return;
+    CU(cudaDeviceSynchronize());
+    for (size_t i = 1; i < trace_name.size(); ++i) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, trace_ev[0], trace_ev[i]));
+      std::fprintf(stderr, "%s %.3f  ", trace_name[i].c_str(), ms);
+    }
+    std::fprintf(stderr, "\n");
+    trace_name.clear();
+  }
+  void design_pair(const double* wd, double* rp, double* ra, double* J) {
+    require_solo();
+    const bool want = rp || ra;
+    if (!design_chunking()) {
+      const double r = design_steps(wd, 1, want);
+      const double q = steps(1, 1, 0, want);
+      if (rp) *rp = r;
+      if (ra) *ra = q;
+      if (J) *J = objective();
+      return;
+    }
+    if (!st_adj) {
+      CU(cudaStreamCreateWithFlags(&st_adj, cudaStreamNonBlocking));
+      ev_prim.resize(kChunks + 1);
+      for (cudaEvent_t& ev : ev_prim) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    long long ib[kChunks + 1];
+    int zb[kChunks + 1];
+    reset_flags();
+    CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long), st));
+    trace("start", st);
+    ensure_h2d();
+    CU(cudaEventRecord(ev_chunk[kChunks], st));  // everything before this call
+    CU(cudaStreamWaitEvent(st_adj, ev_chunk[kChunks], 0));
+    queue_design_upload(wd, ib, zb, false);
+    ++primal_steps;
+    const void* fsrc = f[fc];
+    void* fdst = f[1 - fc];
+    for (int c = 0; c < kChunks; ++c) {
+      const long long m_ = ib[c + 1] - ib[c];
+      if (m_ > 0) {
+        CU(cudaStreamWaitEvent(st, ev_chunk[c], 0));
+        k_scatter_design<<<unsigned((m_ + 255) / 256), 256, 0, st>>>(d_wvals + ib[c], d_design + ib[c],
+                                                                     m_, d_w);
+        ++launches;
+      }
+      SweepArgs sa = sweep(primal_steps, want, nullptr);
+      sa.z0 = zb[c], sa.z1 = zb[c + 1];
+      fast::primal(sa, fsrc, fdst);
+      ++launches;
+      CU(cudaEventRecord(ev_prim[c], st));
+      trace(("P" + std::to_string(c)).c_str(), st);
+    }
+    fc ^= 1;
+    w_host_stale = true;
+    ++adjoint_steps;
+    const void* vsrc = v[vc];
+    void* vdst = v[1 - vc];
+    for (int k = 0; k < kChunks; ++k) {
+      const int c = k < kChunks - 1 ? k + 1 : 0;  // 1, 2, ..., kChunks-1, 0
+      CU(cudaStreamWaitEvent(st_adj, ev_prim[std::min(c + 1, kChunks - 1)], 0));
+      SweepArgs sa = sweep(adjoint_steps, want, d_ring);
+      sa.a.stream = st_adj;
+      sa.z0 = zb[c], sa.z1 = zb[c + 1];
+      if (k < kChunks - 1) sa.n_adj_side = 0;  // the side list once, after every chunk
+      fast::adjoint(sa, f[fc], vsrc, vdst);
+      launches += 1 + (k == kChunks - 1 && sa.n_adj_side > 0);
+      trace(("A" + std::to_string(c)).c_str(), st_adj);
+    }
+    vc ^= 1;
+    CU(cudaEventRecord(ev_prim[kChunks], st_adj));
+    double jv = 0.0;
+    if (J) {  // overlaps the adjoint's tail
+      fast::objective_terms(launch(primal_steps), dim, prec, f[fc], d_support, (long long)support.size(),
+                            d_terms);
+      ++launches;
+      CU(cudaStreamWaitEvent(st, ev_prim[kChunks], 0));
+      jv = pairwise(tree_support, d_terms);
+    } else {
+      CU(cudaStreamWaitEvent(st, ev_prim[kChunks], 0));
+    }
+    CU(cudaGetLastError());
+    reduce_flags(d_flags, 1, false);
+    reduce_flags(d_ring, 1, false);
+    reduce_flags(d_flags + 1, 1, true);
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    sync();  // also: the host design buffer has been consumed when we return
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+    if (rp) *rp = bits_to_double(h_flags[0]);
+    if (ra) *ra = bits_to_double(h_flags[4]);
+    if (J) *J = jv;
+    trace_print();
+  }
+
   // New design values (DesignField::nodes order, host memory) followed by n
   // primal sweeps: optimizer.cpp:200-202 (the MMA update's write-back, then
   // solve_fixed_point). The first sweep runs in z-chunks, each waiting only
@@ -872,29 +1038,10 @@ struct lbgpu_engine {
       return steps(0, nsteps, 0, want_resid);
     }
     if (nsteps <= 0) return 0.0;
-    if (!d_wvals) CU(cudaMalloc(&d_wvals, sizeof(double) * n));
-    if (!st_h2d) {
-      CU(cudaStreamCreateWithFlags(&st_h2d, cudaStreamNonBlocking));
-      ev_chunk.resize(kChunks + 1);
-      for (cudaEvent_t& ev : ev_chunk) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    }
-    reset_flags();
-    // the staging buffer is free once everything queued before us has run
-    CU(cudaEventRecord(ev_chunk[kChunks], st));
-    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
-    const long long plane = (long long)nx * ny;
     long long ib[kChunks + 1];
     int zb[kChunks + 1];
-    for (int c = 0; c <= kChunks; ++c) {
-      zb[c] = int((long long)nz * c / kChunks);
-      ib[c] = std::lower_bound(design.begin(), design.end(), plane * zb[c]) - design.begin();
-    }
-    for (int c = 0; c < kChunks; ++c)
-      if (ib[c + 1] > ib[c]) {
-        CU(cudaMemcpyAsync(d_wvals + ib[c], wd + ib[c], sizeof(double) * (ib[c + 1] - ib[c]),
-                           cudaMemcpyHostToDevice, st_h2d));
-        CU(cudaEventRecord(ev_chunk[c], st_h2d));
-      }
+    reset_flags();
+    queue_design_upload(wd, ib, zb);
     ++primal_steps;
     ++launches;
     const bool r0 = want_resid && nsteps == 1;
@@ -2039,6 +2186,12 @@ int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64
     const double r = e->design_steps(w_design, n, residual != nullptr);
     if (residual) *residual = r;
   });
+}
+
+int lbgpu_pair_step_with_design(lbgpu_engine* e, const double* w_design, double* primal_residual,
+                                double* adjoint_residual, double* objective) {
+  if (!w_design) return LBGPU_E_ARG;
+  return guarded(e, [&] { e->design_pair(w_design, primal_residual, adjoint_residual, objective); });
 }
 
 int lbgpu_tangent_solve(lbgpu_engine* e, const double* dw_design, double d_inlet_dp, double tol,

@@ -1568,7 +1568,9 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
       if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
       if (a.g.x1 > a.g.x0) {
         const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-        dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
+        int nzs = a.g.nz;
+        if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (design pair)
+        dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, nzs);
         k_adjoint<L, R, CK, AK, RES, split, MOM><<<grid, bx, 0, a.stream>>>(a, b, in, out, mom);
       }
     }

@@ -296,6 +296,44 @@ def test_primal_step_with_design_equals_upload_then_step(lbgpu, has_gpu, nz):
         assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
 
 
+@pytest.mark.parametrize("nz", [8, 16, 37])
+def test_pair_step_with_design_equals_separate_calls(lbgpu, has_gpu, nz):
+    """lbgpu_pair_step_with_design (design upload, primal z-chunks and adjoint
+    z-chunks on a second stream, overlapped; nz = 8 takes the fallback, 16 is
+    the smallest chunked lattice, 37 gives uneven chunks) is bitwise
+    primal_step_with_design(1) + adjoint_step(1) + objective: f, v, w,
+    residuals, J, and the gradient taken afterwards."""
+    # design ranges narrower than the lattice
+    wide = {"lattice.nx": 96, "tags.design_x0": 40, "tags.design_x1": 59}
+    wider = {"lattice.nx": 160, "tags.design_x0": 70, "tags.design_x1": 89}
+    for name, over in (("mix3d", {}), ("exch3d", {}), ("bgk3d", {}), ("mix3d", wide),
+                       ("mix3d", wider)):
+        txt = case_text(name, {**over, "lattice.nz": nz})
+        for exact in (False, True):
+            a = lbgpu.Engine.from_config(txt, exact=exact)
+            b = lbgpu.Engine.from_config(txt, exact=exact)
+            for e in (a, b):
+                e.init_state()
+                e.primal_step(20)
+                e.adjoint_step(3)
+            rng = np.random.default_rng(nz)
+            for _ in range(3):
+                vals = rng.uniform(0, 1, a.n_design)
+                rpa, raa, ja = a.pair_step_with_design(vals)
+                rpb = b.primal_step_with_design(vals, 1)
+                rab = b.adjoint_step(1)
+                jb = b.objective()
+                assert (rpa, raa, ja) == (rpb, rab, jb)
+                assert np.array_equal(a.get_state(0), b.get_state(0))
+                assert np.array_equal(a.get_state(1), b.get_state(1))
+                assert np.array_equal(a.design_values(), vals)
+            a.pair_step_with_design(vals, residual=False, objective=False)
+            b.primal_step_with_design(vals, 1, residual=False)
+            b.adjoint_step(1, residual=False)
+            assert np.array_equal(a.get_state(1), b.get_state(1))
+            assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_frozen_base_moment_cache_is_bitwise(lbgpu, has_gpu, name):
     """adjoint_step(n >= 2) and solve_adjoint cache the frozen base's moments

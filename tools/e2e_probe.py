@@ -36,3 +36,6 @@ t("objective", lambda: e.objective())
 t("e2e step (residuals)", lambda: (e.primal_step_with_design(w, 1), e.adjoint_step(1)))
 t("e2e step (J)", lambda: (e.primal_step_with_design(w, 1, residual=False),
                            e.adjoint_step(1, residual=False), e.objective()))
+t("pair_step_with_design (J)", lambda: e.pair_step_with_design(w, residual=False))
+t("pair_step_with_design (no J)", lambda: e.pair_step_with_design(w, residual=False, objective=False))
+t("primal+adjoint no design", lambda: (e.primal_step(1, residual=False), e.adjoint_step(1, residual=False)))
