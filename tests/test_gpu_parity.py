@@ -378,3 +378,28 @@ def test_pair_steps_equal_separate_sweeps(lbgpu, has_gpu, name, exact):
         b.primal_step(1), b.adjoint_step(1)
     assert np.array_equal(a.get_state(1), b.get_state(1))
     assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
+
+
+@pytest.mark.parametrize("name,over", [
+    ("mix3d", {"lattice.nx": 160}),  # rows wider than a block: edge-column blocks
+    ("mix3d", {"lattice.nx": 128}),  # exactly one block per row
+    ("exch3d", {"lattice.nx": 300, "tags.design_x0": 100, "tags.design_x1": 199}),
+    ("grad2d", {"lattice.nx": 257}),
+])
+def test_pair_steps_wide_rows(lbgpu, has_gpu, name, over):
+    """k_pair with its edge columns (inlet / outlet faces) in dedicated blocks
+    is bitwise the sweeps apart, residuals included."""
+    txt = case_text(name, over)
+    a = lbgpu.Engine.from_config(txt)
+    b = lbgpu.Engine.from_config(txt)
+    for e in (a, b):
+        e.init_state()
+        e.primal_step(25)
+    for n in (1, 4):
+        rp, ra = a.pair_steps(n)
+        for _ in range(n):
+            rpb = b.primal_step(1)
+            rab = b.adjoint_step(1)
+        assert (rp, ra) == (rpb, rab)
+        assert np.array_equal(a.get_state(0), b.get_state(0))
+        assert np.array_equal(a.get_state(1), b.get_state(1))
