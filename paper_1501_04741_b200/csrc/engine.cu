@@ -998,27 +998,25 @@ struct lbgpu_engine {
     }
     vc ^= 1;
     CU(cudaEventRecord(ev_prim[kChunks], st_adj));
-    double jv = 0.0;
     if (J) {  // overlaps the adjoint's tail
       fast::objective_terms(launch(primal_steps), dim, prec, f[fc], d_support, (long long)support.size(),
                             d_terms);
       ++launches;
-      CU(cudaStreamWaitEvent(st, ev_prim[kChunks], 0));
-      jv = pairwise(tree_support, d_terms);
-    } else {
-      CU(cudaStreamWaitEvent(st, ev_prim[kChunks], 0));
+      pairwise_queue(tree_support, d_terms);
     }
+    CU(cudaStreamWaitEvent(st, ev_prim[kChunks], 0));
     CU(cudaGetLastError());
     reduce_flags(d_flags, 1, false);
     reduce_flags(d_ring, 1, false);
     reduce_flags(d_flags + 1, 1, true);
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    sync();  // also: the host design buffer has been consumed when we return
+    if (J) CU(cudaMemcpyAsync(h_flags + 5, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();  // one host sync per call; the host design buffer is consumed too
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
     if (rp) *rp = bits_to_double(h_flags[0]);
     if (ra) *ra = bits_to_double(h_flags[4]);
-    if (J) *J = jv;
+    if (J) *J = bits_to_double(h_flags[5]);
     trace_print();
   }
 
@@ -1393,6 +1391,14 @@ struct lbgpu_engine {
 
   // ------------------------------------------------------- reductions
   double pairwise(PairTree& tr, const double* d_t) {
+    pairwise_queue(tr, d_t);
+    double out = 0.0;
+    CU(cudaMemcpyAsync(&out, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();
+    return out;
+  }
+  // the tree replay only; the sum lands in d_scalar[0]
+  void pairwise_queue(PairTree& tr, const double* d_t) {
     const int nb = (tr.leaves + 127) / 128;
     k_leaf_sums<<<nb, 128, 0, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_vals);
     for (int h = 1; h <= tr.top; ++h) {
@@ -1402,10 +1408,6 @@ struct lbgpu_engine {
     k_combine_top<<<1, 1024, 0, st>>>(tr.d_vals, tr.d_ops, tr.d_lvl, tr.leaves, tr.top,
                                       int(tr.lvl.size()) - 1, tr.ops, d_scalar);
     launches += 2 + tr.top;
-    double out = 0.0;
-    CU(cudaMemcpyAsync(&out, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
-    sync();
-    return out;
   }
   double objective(const void* buf = nullptr) {
     const Launch a = launch(primal_steps);
