@@ -74,6 +74,13 @@ typedef struct {
    * columns: owned at 0..span-1, right ghost at span, left ghost at nxl-1;
    * support indices are local. nx stays the global extent. */
   int slab_count, slab_id;
+  /* State storage (no reference counterpart: StateField<R> always double-
+   * buffers, lattice.hpp:57-92). 0: two buffers per field (every operation).
+   * 1: in-place AA-pattern streaming, one buffer per field (half the memory,
+   * the same bytes per sweep): fixed-step sweeps, pairs, objective and
+   * gradient only -- no step residual, hence no tol-stop solves (product
+   * build only). */
+  int streaming;
 } lbgpu_system_desc;
 
 /* One monitoring row (run_record.hpp:11-19): iteration, residual,
@@ -99,6 +106,12 @@ int lbgpu_create_from_config(const char* cfg_text, const char* overrides, int de
 /* One x-slab of the case: decompose(nx, slab_count)[slab_id] with local tables. */
 int lbgpu_create_slab_from_config(const char* cfg_text, const char* overrides, int device,
                                   int exact, int slab_count, int slab_id, lbgpu_engine** out);
+/* Both of the above with the storage choice (lbgpu_system_desc::streaming):
+ * slab_count 1 and slab_id 0 is the whole lattice, slab_id -1 one slab in the
+ * ghost-column layout (a single-rank ring). */
+int lbgpu_create_from_config_ex(const char* cfg_text, const char* overrides, int device,
+                                int exact, int slab_count, int slab_id, int streaming,
+                                lbgpu_engine** out);
 void lbgpu_destroy(lbgpu_engine* e);
 /* Host-only: the System build_case would assemble from this case text, in
  * reference form (tags, bc arrays, design w/mask/nodes, support, A), without
@@ -172,6 +185,19 @@ int lbgpu_tangent_solve(lbgpu_engine* e, const double* dw_design, double d_inlet
  * write (no clamp), as in the reference. State, design and model are restored. */
 int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, int64_t max_iter,
                       int64_t fixed_iters, double* out);
+/* n fd_gradient components at once (grad_check_impl's 12 components x 3
+ * steps, case.cpp:256-283, as one call): out[k] = the central difference along
+ * ordinals[k] with step steps[k]. With fixed_iters >= 0 every side is queued
+ * on the device back to back -- raw write of the perturbed w (or rho_in), the
+ * start state, fixed_iters sweeps, evaluate_raw into a device slot,
+ * write-back -- with one host sync for the whole batch; with fixed_iters < 0
+ * each side is a tol-stop solve. from_state 0: each side starts from
+ * initialize_state (bitwise lbgpu_fd_gradient per component); 1 (fixed_iters
+ * >= 0 only): from the engine's current primal state -- the finite-difference
+ * check of lbgpu_unsteady_adjoint run from a developed state. */
+int lbgpu_fd_gradient_batch(lbgpu_engine* e, int64_t n, const int64_t* ordinals,
+                            const double* steps, double tol, int64_t max_iter,
+                            int64_t fixed_iters, int from_state, double* out);
 /* optimizer.cpp:200-202: write new design values (DesignField::nodes order,
  * host memory; pinned overlaps best) into w, then n >= 1 primal steps. The
  * upload is pipelined under the first sweep in z-chunks. Equivalent to

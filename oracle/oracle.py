@@ -28,6 +28,8 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.isdir(os.path.join(REF_SRC, "src")):
         targets.append("ref")
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1501_04741_b200", "liblbgpu.so")):
+            targets.append("drop_in")  # the reference-side binding
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 
@@ -310,6 +312,8 @@ def _load_ref():
         L.ref_partition_check.argtypes = [vp, C.c_int, C.c_long, C.POINTER(C.c_double),
                                           C.POINTER(C.c_double)]
         L.ref_time.argtypes = [vp, C.c_int, C.c_int, C.c_long, C.POINTER(C.c_double)]
+        L.ref_partitioned.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, _DP]
+        L.ref_objective_enabled.argtypes = [vp, C.c_int]
         L.ref_tangent.argtypes = [vp, vp, C.c_double, C.c_double, C.c_long,
                                   C.POINTER(C.c_double), C.POINTER(C.c_long),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -453,6 +457,21 @@ class RefOracle:
         a, b = C.c_double(), C.c_double()
         self._ok(self.L.ref_partition_check(self.h, parts, steps, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def partitioned(self, threads: int, n_primal: int = 0, n_adjoint: int = 0,
+                    n_pairs: int = 0):
+        """The reference's PartitionedRun on `threads` host threads from the
+        handle's f with v = 0: n_primal primal steps, n_adjoint adjoint steps,
+        n_pairs (primal, adjoint) pairs; f and v gathered back. Returns the
+        last primal and adjoint residuals."""
+        r = np.zeros(2)
+        self._ok(self.L.ref_partitioned(self.h, threads, n_primal, n_adjoint, n_pairs, r))
+        return float(r[0]), float(r[1])
+
+    def objective_enabled(self, on: bool) -> None:
+        """obj_empty of the A14 composition recipe: adjoint steps without
+        the objective source while off."""
+        self._ok(self.L.ref_objective_enabled(self.h, 1 if on else 0))
 
     def time_steps(self, which: int, threads: int, steps: int) -> float:
         s = C.c_double()

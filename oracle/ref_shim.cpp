@@ -16,6 +16,7 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <algorithm>
 #include <variant>
 
 #include "lbopt/adjoint.hpp"
@@ -363,6 +364,51 @@ int ref_time(void* h, int which, int threads, long steps, double* seconds) {
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
       }
     }, H(h)->fl);
+  });
+}
+
+// Full-size parity oracle: the reference's thread-per-slab runner
+// (PartitionedRun, partition.cpp:93-253; bitwise equal to the monolithic
+// operators, test_partition.cpp:53-141) over the handle's state. Loads the
+// handle's f, zeroes v, runs n_primal primal lock steps, then n_adjoint
+// adjoint lock steps against the state the slabs hold, then n_pairs
+// (primal, adjoint) pairs, and gathers f and v back into the handle.
+// resid[0] / resid[1]: last_residual() after the last primal / adjoint step.
+int ref_partitioned(void* h, int threads, long n_primal, long n_adjoint, long n_pairs,
+                    double* resid) {
+  return guard([&] {
+    std::visit([&](auto& F) {
+      using R = std::decay_t<decltype(F.f.raw(0)[0])>;
+      PartitionedRun<R> run(H(h)->bc.sys, H(h)->bc.objective, threads);
+      run.load_state(F.f);
+      run.reset_adjoint();
+      double rp = 0.0, ra = 0.0;
+      for (long i = 0; i < n_primal; ++i) run.step_primal();
+      if (n_primal > 0) rp = run.last_residual();
+      for (long i = 0; i < n_adjoint; ++i) run.step_adjoint();
+      if (n_adjoint > 0) ra = run.last_residual();
+      for (long i = 0; i < n_pairs; ++i) {
+        run.step_primal();
+        if (i == n_pairs - 1) rp = run.last_residual();
+        run.step_adjoint();
+      }
+      if (n_pairs > 0) ra = run.last_residual();
+      run.gather_state(F.f);
+      run.gather_adjoint(F.v);
+      if (resid) resid[0] = rp, resid[1] = ra;
+    }, H(h)->fl);
+  });
+}
+
+// The A14 composition recipe's obj_empty: on = 0 clears the
+// objective's full-grid membership flags so adjoint_step skips the source
+// term (adjoint.cpp:199); on = 1 restores them from the support list.
+int ref_objective_enabled(void* h, int on) {
+  return guard([&] {
+    ObjectiveSpec& ob = H(h)->bc.objective;
+    std::fill(ob.on_support.begin(), ob.on_support.end(), std::uint8_t(0));
+    if (on)
+      for (long i : ob.support) ob.on_support[std::size_t(i)] = 1;
   });
 }
 

@@ -61,6 +61,7 @@ class SystemDesc(C.Structure):
         ("obj_kind", C.c_int), ("flux_axis", C.c_int), ("flux_sign", C.c_int),
         ("support", C.c_void_p), ("n_support", C.c_int64),
         ("slab_count", C.c_int), ("slab_id", C.c_int),
+        ("streaming", C.c_int),
     ]
 
 
@@ -87,6 +88,8 @@ def load_library() -> C.CDLL:
     L.lbgpu_error_message.argtypes = [vp]
     L.lbgpu_create.argtypes = [C.POINTER(SystemDesc), C.POINTER(vp)]
     L.lbgpu_create_from_config.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
+    L.lbgpu_create_from_config_ex.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                              C.c_int, C.c_int, C.POINTER(vp)]
     L.lbgpu_destroy.argtypes = [vp]
     L.lbgpu_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(i64)]
     L.lbgpu_get_tables.argtypes = [vp] + [vp] * 9
@@ -108,6 +111,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_pair_step_with_design.argtypes = [vp, vp, dp, dp, dp]
     L.lbgpu_time_pair_steps.argtypes = [vp, i64, dp]
     L.lbgpu_fd_gradient.argtypes = [vp, i64, C.c_double, C.c_double, i64, i64, dp]
+    L.lbgpu_fd_gradient_batch.argtypes = [vp, i64, vp, vp, C.c_double, i64, i64, C.c_int, vp]
     L.lbgpu_tangent_solve.argtypes = [vp, vp, C.c_double, C.c_double, i64, dp, C.POINTER(i64), dp,
                                       C.POINTER(C.c_int)]
     L.lbgpu_adjoint_step.argtypes = [vp, i64, C.c_int, dp]
@@ -159,12 +163,22 @@ class Engine:
     # --- construction -------------------------------------------------------
     @classmethod
     def from_config(cls, cfg_text: str, overrides: dict | None = None, device: int = 0,
-                    exact: bool = False) -> "Engine":
-        """CaseConfig text (+ dotted overrides) -> build_case -> engine."""
+                    exact: bool = False, streaming: str = "double") -> "Engine":
+        """CaseConfig text (+ dotted overrides) -> build_case -> engine.
+        streaming: "double" (two state buffers per field, every operation) or
+        "aa" (in place, one buffer per field: fixed-step sweeps, pairs,
+        objective and gradient only)."""
+        return cls._create(cfg_text, overrides, device, exact, 1, 0, streaming)
+
+    @classmethod
+    def _create(cls, cfg_text, overrides, device, exact, slab_count, slab_id, streaming):
         L = load_library()
         ov = "\n".join(f"{k}={v}" for k, v in (overrides or {}).items()).encode()
+        if streaming not in ("double", "aa"):
+            raise LbgpuError(E_ARG, f"streaming must be 'double' or 'aa', not {streaming!r}")
         h = C.c_void_p()
-        rc = L.lbgpu_create_from_config(cfg_text.encode(), ov, device, int(exact), C.byref(h))
+        rc = L.lbgpu_create_from_config_ex(cfg_text.encode(), ov, device, int(exact), slab_count,
+                                           slab_id, int(streaming == "aa"), C.byref(h))
         if rc:
             raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
         return cls(h.value)
@@ -174,7 +188,8 @@ class Engine:
                     nu=0.02, beta_fluid=0.003, beta_solid=0.003, inlet_dp=0.0, u_clamp=0.05,
                     omega_nonhydro=1.0, switch_theta=3.0, fluid_power=False, bgk=False,
                     obj_kind=0, precision=64, exact=False, device=0, A=None, vel=None,
-                    opp=None) -> "Engine":
+                    opp=None, relax=None, flux_axis=0, flux_sign=1,
+                    streaming: str = "double") -> "Engine":
         """Flattened System arrays (the drop-in seam fed by the reference's own
         System)."""
         L = load_library()
@@ -195,12 +210,14 @@ class Engine:
         d.u_clamp, d.omega_nonhydro, d.switch_theta = u_clamp, omega_nonhydro, switch_theta
         d.switch_form = int(fluid_power)
         d.A = arr(A, np.float64)
+        d.relax = arr(relax, np.float64)
         d.vel = arr(vel, np.int32)
         d.opp = arr(opp, np.int32)
         d.tag, d.bc_T = arr(tag, np.uint8), arr(bc_T, np.float64)
         d.bc_axis, d.bc_sign = arr(bc_axis, np.int8), arr(bc_sign, np.int8)
         d.w, d.design_mask = arr(w, np.float64), arr(mask, np.uint8)
-        d.obj_kind, d.flux_axis, d.flux_sign = obj_kind, 0, 1
+        d.obj_kind, d.flux_axis, d.flux_sign = obj_kind, flux_axis, flux_sign
+        d.streaming = int(streaming == "aa")
         d.support = arr(support, np.int64)
         d.n_support = len(support)
         h = C.c_void_p()
@@ -211,16 +228,11 @@ class Engine:
 
     @classmethod
     def slab_from_config(cls, cfg_text: str, overrides: dict | None, slab_count: int,
-                         slab_id: int, device: int = 0, exact: bool = False) -> "Engine":
-        """Slab `slab_id` of decompose(nx, slab_count) (partition.cpp:9-21)."""
-        L = load_library()
-        ov = "\n".join(f"{k}={v}" for k, v in (overrides or {}).items()).encode()
-        h = C.c_void_p()
-        rc = L.lbgpu_create_slab_from_config(cfg_text.encode(), ov, device, int(exact),
-                                             slab_count, slab_id, C.byref(h))
-        if rc:
-            raise LbgpuError(rc, L.lbgpu_last_create_error().decode())
-        return cls(h.value)
+                         slab_id: int, device: int = 0, exact: bool = False,
+                         streaming: str = "double") -> "Engine":
+        """Slab `slab_id` of decompose(nx, slab_count) (partition.cpp:9-21);
+        slab_id -1 with slab_count 1: the whole lattice in ghost layout."""
+        return cls._create(cfg_text, overrides, device, exact, slab_count, slab_id, streaming)
 
     def slab(self) -> dict:
         v = (C.c_int * 6)()
@@ -347,6 +359,19 @@ class Engine:
         self._ok(self.L.lbgpu_fd_gradient(self.h, ordinal, h, tol, max_iter, fixed_iters,
                                           C.byref(out)))
         return out.value
+
+    def fd_gradient_batch(self, ordinals, steps, tol: float = 0.0, max_iter: int = 200000,
+                          fixed_iters: int = -1, from_state: bool = False) -> np.ndarray:
+        """fd_gradient for many (ordinal, step) components in one call (one
+        host sync with fixed_iters >= 0); from_state: each side restarts from
+        the current primal state instead of initialize_state."""
+        o = np.ascontiguousarray(ordinals, np.int64)
+        h = np.ascontiguousarray(steps, np.float64)
+        assert o.size == h.size
+        out = np.zeros(max(o.size, 1))
+        self._ok(self.L.lbgpu_fd_gradient_batch(self.h, o.size, _ptr(o), _ptr(h), tol, max_iter,
+                                                fixed_iters, int(from_state), _ptr(out)))
+        return out[: o.size]
 
     def tangent_solve(self, dw: np.ndarray, d_inlet_dp: float, tol: float,
                       max_iter: int = 200000) -> tuple[float, int, float, bool]:

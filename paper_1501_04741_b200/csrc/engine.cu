@@ -88,6 +88,7 @@ const Nccl& nccl() {
 
 constexpr unsigned long long kNoBad = ~0ull;
 constexpr unsigned long long kIdxMask = (1ull << 40) - 1;
+constexpr unsigned long long kKeyStepMask = (1ull << 24) - 1;  // step field of a bad-node key
 
 // ------------------------------------------------------------ tables
 // Full-pivot Gauss-Jordan inverse (the same elimination order as the oracle
@@ -286,6 +287,18 @@ struct lbgpu_engine {
   // in-process P2P group (one stream per slab, any devices; the sweeps push
   // their boundary planes into the neighbours' ghosts)
   int xmode = 0;
+  // In-place AA streaming (lbgpu_system_desc::streaming): f[1] == f[0] and
+  // v[1] == v[0]; fpar / vpar = the current layout of each (0: O, the
+  // reference layout; 1: E) -- kernels.cuh FM_O / FM_E.
+  int aa = 0, fpar = 0, vpar = 0;
+  int fmode() const { return aa ? 1 + fpar : 0; }
+  int vmode() const { return aa ? 1 + vpar : 0; }
+  void require_db(const char* what) const {
+    if (aa)
+      throw Fail{LBGPU_E_STATE, std::string(what) +
+                                    " needs the double-buffered state (in-place streaming keeps "
+                                    "no previous state for the step residual)"};
+  }
   void* push_dst_l = nullptr;  // xmode 3: this sweep's neighbour destinations
   void* push_dst_r = nullptr;
   cudaEvent_t ev_step[2] = {nullptr, nullptr};  // xmode 3: sweep k done (parity k)
@@ -341,6 +354,10 @@ struct lbgpu_engine {
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long primal_steps = 0, adjoint_steps = 0, tangent_steps = 0;
+  // Step keys of bad-node reports are relative to these (set by reset_flags,
+  // and per batch in solve()), so a key's 24-bit step field never wraps over
+  // an engine's lifetime; reports add the caller's iteration offset.
+  long long kb_p = 0, kb_a = 0, kb_t = 0;
   long long launches = 0;  // kernels this engine launched (sweeps + reductions + layout)
   std::vector<cudaEvent_t> evs;  // per-sweep timing events (lbgpu_time_pairs)
   std::string err;
@@ -362,6 +379,7 @@ struct lbgpu_engine {
     if (st_adj) cudaStreamDestroy(st_adj);
     for (void* h : halo_buf) cudaFree(h);
     if (device >= 0) cudaSetDevice(device);
+    if (aa) f[1] = v[1] = nullptr;  // aliases of f[0] / v[0]
     for (void* p : {f[0], f[1], v[0], v[1], snap, tg[0], tg[1]}) cudaFree(p);
     cudaFree(d_dw), cudaFree(d_mom);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
@@ -372,6 +390,7 @@ struct lbgpu_engine {
     if (h_flags) cudaFreeHost(h_flags);
     tree_support.release(), tree_design.release(), tree_inlet.release();
     for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : trace_ev) cudaEventDestroy(ev);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (st && owns_stream) cudaStreamDestroy(st);
@@ -388,6 +407,10 @@ struct lbgpu_engine {
         (!d.support && d.n_support > 0))
       throw Fail{LBGPU_E_ARG, "system description is missing a per-node table"};
     nx = d.nx, ny = d.ny, nz = d.nz, prec = d.precision, exact = d.exact ? 1 : 0;
+    if (d.streaming != 0 && d.streaming != 1) throw Fail{LBGPU_E_CONFIG, "streaming must be 0 or 1"};
+    aa = d.streaming;
+    if (aa && exact)
+      throw Fail{LBGPU_E_CONFIG, "in-place streaming is a product-build mode (not the bit-exact build)"};
     device = d.device;
     gnx = d.nx;
     slab_count = d.slab_count > 1 ? d.slab_count : 1;
@@ -453,11 +476,12 @@ struct lbgpu_engine {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     const size_t fb = field_bytes();
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < (aa ? 1 : 2); ++b) {
       CU(cudaMalloc(&f[b], fb));
       CU(cudaMalloc(&v[b], fb));
       CU(cudaMemset(v[b], 0, fb));
     }
+    if (aa) f[1] = f[0], v[1] = v[0];
     CU(cudaMalloc(&d_code, N));
     CU(cudaMalloc(&d_w, sizeof(double) * N));
     CU(cudaMalloc(&d_bcT, sizeof(double) * N));
@@ -568,6 +592,8 @@ struct lbgpu_engine {
     M.rho_in = 1.0 + 3.0 * d.inlet_dp;
     M.rho_out = 1.0;
     M.u_clamp = d.u_clamp;
+    M.inv_rho_in = 1.0 / M.rho_in, M.inv_rho_out = 1.0 / M.rho_out;
+    M.inv_1m_uc = 1.0 / (1.0 - d.u_clamp), M.inv_1p_uc = 1.0 / (1.0 + d.u_clamp);
     M.theta = d.switch_theta;
     M.theta_int = (d.switch_theta == std::floor(d.switch_theta) && d.switch_theta >= 1 &&
                    d.switch_theta <= 16) ? int(d.switch_theta) : 0;
@@ -633,10 +659,14 @@ struct lbgpu_engine {
   }
 
   // ------------------------------------------------------------ helpers
+  // d_flags: [0] residual, [1] first bad node (primal, or the call's only
+  // sweep kind), [2] aux, [3] first bad node of the adjoint half of a pair call
   void reset_flags() {
-    const unsigned long long init[4] = {0ull, kNoBad, 0ull, 0ull};
+    const unsigned long long init[4] = {0ull, kNoBad, 0ull, kNoBad};
     CU(cudaMemcpyAsync(d_flags, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    kb_p = primal_steps, kb_a = adjoint_steps, kb_t = tangent_steps;
   }
+  // step: the sweep's number relative to the current key base (1-based)
   Launch launch(unsigned long long step) const {
     Launch a;
     a.g = G;
@@ -645,7 +675,7 @@ struct lbgpu_engine {
     a.fl.resid = d_flags;
     a.fl.bad = d_flags + 1;
     a.fl.aux = d_flags + 2;
-    a.fl.step_key = step << 40;
+    a.fl.step_key = (step & kKeyStepMask) << 40;
     a.stream = st;
     return a;
   }
@@ -656,6 +686,7 @@ struct lbgpu_engine {
     s.dim = dim, s.prec = prec, s.ck = ck, s.resid = resid;
     s.adj_side = d_adj_side, s.n_adj_side = (long long)adj_side.size();
     s.part = 0;
+    s.fm = fmode(), s.vm = vmode();
     return s;
   }
   void sync() { CU(cudaStreamSynchronize(st)); }
@@ -663,10 +694,11 @@ struct lbgpu_engine {
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
     sync();
   }
-  // NumericError with the reference's message shape (collision.cpp:355-361, 387-389).
-  void raise_bad(unsigned long long key, const char* what) {
+  // NumericError with the reference's message shape (collision.cpp:355-361,
+  // 387-389): the iteration is `base` plus the key's call-relative step.
+  void raise_bad(unsigned long long key, const char* what, long long base = 0) {
     const long long gidx = (long long)(key & kIdxMask);
-    const long long step = (long long)(key >> 40);
+    const long long step = base + (long long)(key >> 40);
     // keys hold the GLOBAL flat index (gflat): decode with the global x extent
     const int x = int(gidx % gnx), y = int((gidx / gnx) % ny), z = int(gidx / ((long long)gnx * ny));
     reset_flags();
@@ -687,13 +719,15 @@ struct lbgpu_engine {
   // ------------------------------------------------------------ sweeps
   // NCCL mode: the two boundary columns first, their halo on the comm stream
   // while the interior columns compute, joined before the next sweep.
+  // kind: the exchange after the sweep (0 double-buffered; in place: 1 forward
+  // after a sweep from O, 2 reverse after a sweep from E; kernels.cuh)
   template <class F>
-  void overlapped(int field, void* dst, SweepArgs s, F&& launch_part) {
+  void overlapped(int field, void* dst, SweepArgs s, F&& launch_part, int kind = 0) {
     s.part = 2;
     launch_part(s);
     CU(cudaEventRecord(ev_bnd, st));
     CU(cudaStreamWaitEvent(st_comm, ev_bnd, 0));
-    nccl_exchange(field, dst, st_comm);
+    nccl_exchange(field, dst, st_comm, kind);
     CU(cudaEventRecord(ev_halo, st_comm));
     s.part = 1;
     launch_part(s);
@@ -705,7 +739,15 @@ struct lbgpu_engine {
   void primal_raw(const void* src, void* dst, bool resid, unsigned long long* slot, bool exch) {
     ++primal_steps;
     ++launches;
-    SweepArgs s = sweep(primal_steps, resid, slot);
+    SweepArgs s = sweep(primal_steps - kb_p, resid, slot);
+    if (aa) {
+      if (resid) require_db("a step residual");
+      auto go = [&](const SweepArgs& a) { fast::primal_aa(a, dst); };
+      if (exch && xmode == 2) overlapped(0, dst, s, go, 1 + fpar);
+      else go(s);
+      fpar ^= 1;
+      return;
+    }
     s.a.push = push_targets();
     auto go = [&](const SweepArgs& a) {
       if (exact) exact::primal(a, src, dst);
@@ -719,9 +761,18 @@ struct lbgpu_engine {
                    unsigned long long* slot, bool exch) {
     ++adjoint_steps;
     ++launches;
-    SweepArgs s = sweep(adjoint_steps, resid, slot);
-    s.a.push = push_targets();
+    SweepArgs s = sweep(adjoint_steps - kb_a, resid, slot);
     if (kernel == 0 && mom_base && mom_base == base) s.mom = d_mom;
+    if (aa) {
+      if (resid) require_db("a step residual");
+      if (kernel != 0) require_db("the dual-sweep adjoint kernel");
+      auto go = [&](const SweepArgs& a) { fast::adjoint_aa(a, base, dst); };
+      if (exch && xmode == 2) overlapped(1, dst, s, go, 1 + vpar);
+      else go(s);
+      vpar ^= 1;
+      return;
+    }
+    s.a.push = push_targets();
     auto go = [&](const SweepArgs& a) {
       if (kernel) {
         if (exact) exact::adjoint_dual(a, base, src, dst);
@@ -738,7 +789,7 @@ struct lbgpu_engine {
   void tangent_launch(bool resid, unsigned long long* slot) {
     ++tangent_steps;
     ++launches;
-    const SweepArgs s = sweep(tangent_steps, resid, slot);
+    const SweepArgs s = sweep(tangent_steps - kb_t, resid, slot);
     if (exact) exact::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
     else fast::tangent(s, f[fc], tg[tc], tg[1 - tc], d_dw, tangent_drho);
     tc ^= 1;
@@ -762,6 +813,9 @@ struct lbgpu_engine {
   // ------------------------------------------------------------ halo
   void* cur(int field) const { return field == 0 ? f[fc] : v[vc]; }
   size_t halo_bytes() const { return bytes_per_real() * 6 * size_t(ny) * nz; }
+  // one sweep's exchange for field `field` with pack / unpack ops of `kind`
+  static int pack_op(int kind) { return kind == 0 ? 0 : kind == 1 ? 5 : 3; }
+  static int unpack_op(int kind) { return kind == 0 ? 1 : kind == 1 ? 6 : 4; }
   void ensure_halo_bufs() {
     for (void*& h : halo_buf)
       if (!h) CU(cudaMalloc(&h, halo_bytes()));
@@ -786,10 +840,10 @@ struct lbgpu_engine {
     }
   }
   // pack -> NCCL send/recv with both neighbours -> unpack, all on stream S.
-  void nccl_exchange(int field, void* buf, cudaStream_t S) {
+  void nccl_exchange(int field, void* buf, cudaStream_t S, int kind = 0) {
     {
       ensure_halo_bufs();
-      halo_op(0, field, halo_buf[0], halo_buf[1], nullptr, nullptr, buf, S);
+      halo_op(pack_op(kind), field, halo_buf[0], halo_buf[1], nullptr, nullptr, buf, S);
       const size_t cnt = halo_bytes() / bytes_per_real();
       const ncclDataType_t ty = prec == 64 ? ncclFloat64 : ncclFloat32;
       const int left = (rank - 1 + nranks) % nranks, right = (rank + 1) % nranks;
@@ -803,7 +857,7 @@ struct lbgpu_engine {
       N_.Recv(halo_buf[3], cnt, ty, right, comm, S);
       const ncclResult_t r = N_.GroupEnd();
       if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + N_.GetErrorString(r)};
-      halo_op(1, field, halo_buf[2], halo_buf[3], nullptr, nullptr, buf, S);
+      halo_op(unpack_op(kind), field, halo_buf[2], halo_buf[3], nullptr, nullptr, buf, S);
     }
   }
   // Global max / min of device flag words across ranks (NCCL mode).
@@ -823,8 +877,9 @@ struct lbgpu_engine {
     else fast::init_state(N, dim, prec, f[fc], st);
     // ghost layout: sweeps write owned columns only, so both ping-pong buffers
     // carry the same ghost columns until an exchange refreshes them
-    if (ghosts) CU(cudaMemcpyAsync(f[1 - fc], f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
+    if (ghosts && !aa) CU(cudaMemcpyAsync(f[1 - fc], f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
+    fpar = vpar = 0;  // uniform planes (and zeros): layout O
     CU(cudaGetLastError());
   }
 
@@ -836,7 +891,8 @@ struct lbgpu_engine {
     MomScope(lbgpu_engine* e_, long long n, int kernel) : e(e_) {
       if (e->exact || kernel != 0 || n < 2) return;
       if (!e->d_mom) CU(cudaMalloc(&e->d_mom, e->bytes_per_real() * size_t(e->dim + 7) * e->N));
-      fast::base_moments(e->launch(e->adjoint_steps), e->dim, e->prec, e->f[e->fc], e->d_mom);
+      fast::base_moments(e->launch(e->adjoint_steps - e->kb_a), e->dim, e->prec, e->fmode(),
+                         e->f[e->fc], e->d_mom);
       CU(cudaGetLastError());
       ++e->launches;
       e->mom_base = e->f[e->fc];
@@ -846,6 +902,7 @@ struct lbgpu_engine {
 
   double steps(int which, long long n, int kernel, bool want_resid) {
     require_solo();
+    if (want_resid) require_db("a step residual");
     if (n <= 0) return 0.0;
     reset_flags();
     MomScope ms(this, which == 1 ? n : 0, kernel);
@@ -916,9 +973,12 @@ struct lbgpu_engine {
   // LBGPU_TRACE_PAIR=1: print each pipeline stage's finish time (development).
   std::vector<cudaEvent_t> trace_ev;
   std::vector<std::string> trace_name;
-  void trace(const char* what, cudaStream_t s_) {
+  static bool trace_on() {
     static const bool on = std::getenv("LBGPU_TRACE_PAIR") != nullptr;
-    if (!on) return;
+    return on;
+  }
+  void trace(const char* what, cudaStream_t s_) {
+    if (!trace_on()) return;
     if (trace_ev.size() <= trace_name.size()) {
       trace_ev.emplace_back();
       CU(cudaEventCreate(&trace_ev.back()));
@@ -939,6 +999,7 @@ struct lbgpu_engine {
   }
   void design_pair(const double* wd, double* rp, double* ra, double* J) {
     require_solo();
+    require_db("the pipelined design pair");
     const bool want = rp || ra;
     if (!design_chunking()) {
       const double r = design_steps(wd, 1, want);
@@ -957,6 +1018,7 @@ struct lbgpu_engine {
     int zb[kChunks + 1];
     reset_flags();
     CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long), st));
+    trace_name.clear();  // a call that raised before trace_print left its names
     trace("start", st);
     ensure_h2d();
     CU(cudaEventRecord(ev_chunk[kChunks], st));  // everything before this call
@@ -973,12 +1035,12 @@ struct lbgpu_engine {
                                                                      m_, d_w);
         ++launches;
       }
-      SweepArgs sa = sweep(primal_steps, want, nullptr);
+      SweepArgs sa = sweep(primal_steps - kb_p, want, nullptr);
       sa.z0 = zb[c], sa.z1 = zb[c + 1];
       fast::primal(sa, fsrc, fdst);
       ++launches;
       CU(cudaEventRecord(ev_prim[c], st));
-      trace(("P" + std::to_string(c)).c_str(), st);
+      if (trace_on()) trace(("P" + std::to_string(c)).c_str(), st);
     }
     fc ^= 1;
     w_host_stale = true;
@@ -988,19 +1050,20 @@ struct lbgpu_engine {
     for (int k = 0; k < kChunks; ++k) {
       const int c = k < kChunks - 1 ? k + 1 : 0;  // 1, 2, ..., kChunks-1, 0
       CU(cudaStreamWaitEvent(st_adj, ev_prim[std::min(c + 1, kChunks - 1)], 0));
-      SweepArgs sa = sweep(adjoint_steps, want, d_ring);
+      SweepArgs sa = sweep(adjoint_steps - kb_a, want, d_ring);
       sa.a.stream = st_adj;
+      sa.a.fl.bad = d_flags + 3;  // the adjoint half reports after the primal's
       sa.z0 = zb[c], sa.z1 = zb[c + 1];
       if (k < kChunks - 1) sa.n_adj_side = 0;  // the side list once, after every chunk
       fast::adjoint(sa, f[fc], vsrc, vdst);
       launches += 1 + (k == kChunks - 1 && sa.n_adj_side > 0);
-      trace(("A" + std::to_string(c)).c_str(), st_adj);
+      if (trace_on()) trace(("A" + std::to_string(c)).c_str(), st_adj);
     }
     vc ^= 1;
     CU(cudaEventRecord(ev_prim[kChunks], st_adj));
     if (J) {  // overlaps the adjoint's tail
-      fast::objective_terms(launch(primal_steps), dim, prec, f[fc], d_support, (long long)support.size(),
-                            d_terms);
+      fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support, (long long)support.size(),
+                            d_terms, 0);
       ++launches;
       pairwise_queue(tree_support, d_terms);
     }
@@ -1009,15 +1072,19 @@ struct lbgpu_engine {
     reduce_flags(d_flags, 1, false);
     reduce_flags(d_ring, 1, false);
     reduce_flags(d_flags + 1, 1, true);
+    reduce_flags(d_flags + 3, 1, true);
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (J) CU(cudaMemcpyAsync(h_flags + 5, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
     sync();  // one host sync per call; the host design buffer is consumed too
+    trace_print();
+    // the primal's failure first (the three-call sequence raises before its
+    // adjoint runs); on either error the adjoint half has already advanced v
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+    if (h_flags[3] != kNoBad) raise_bad(h_flags[3], "adjoint iteration");
     if (rp) *rp = bits_to_double(h_flags[0]);
     if (ra) *ra = bits_to_double(h_flags[4]);
     if (J) *J = bits_to_double(h_flags[5]);
-    trace_print();
   }
 
   // New design values (DesignField::nodes order, host memory) followed by n
@@ -1030,6 +1097,7 @@ struct lbgpu_engine {
   static constexpr int kChunks = 8;
   double design_steps(const double* wd, long long nsteps, bool want_resid) {
     require_solo();
+    require_db("the pipelined design upload");
     const long long n = (long long)design.size();
     if (!n || exact || dim == 2 || xmode == 2 || nz < 2 * kChunks) {
       upload_design_values(wd);
@@ -1050,7 +1118,7 @@ struct lbgpu_engine {
         k_scatter_design<<<unsigned((m_ + 255) / 256), 256, 0, st>>>(d_wvals + ib[c], d_design + ib[c],
                                                                      m_, d_w);
       }
-      SweepArgs sa = sweep(primal_steps, r0, nullptr);
+      SweepArgs sa = sweep(primal_steps - kb_p, r0, nullptr);
       sa.z0 = zb[c], sa.z1 = zb[c + 1];
       if (exact) exact::primal(sa, f[fc], f[1 - fc]);
       else fast::primal(sa, f[fc], f[1 - fc]);
@@ -1091,12 +1159,35 @@ struct lbgpu_engine {
   // f^{n+1} gathered once, FP64); otherwise the sweeps run apart. Residuals
   // (nullable) are those of the last pair.
   // Fused pairs win at FP64 only (FP32 measured slower than the sweeps apart).
-  bool fuse_pairs() const { return !exact && prec == 64; }
+  bool fuse_pairs() const { return !exact && (prec == 64 || aa); }
   void fused_pair_raw(bool resid) {
     ++primal_steps;
     ++adjoint_steps;
     ++launches;
-    SweepArgs s = sweep(primal_steps, resid, nullptr);
+    SweepArgs s = sweep(primal_steps - kb_p, resid, nullptr);
+    if (aa) {
+      if (resid) require_db("a step residual");
+      auto go = [&](const SweepArgs& a) { fast::pair_aa(a, f[0], v[0]); };
+      if (xmode == 2) {
+        SweepArgs b = s;
+        b.part = 2;
+        go(b);
+        CU(cudaEventRecord(ev_bnd, st));
+        CU(cudaStreamWaitEvent(st_comm, ev_bnd, 0));
+        nccl_exchange(0, f[0], st_comm, 1 + fpar);
+        nccl_exchange(1, v[0], st_comm, 1 + vpar);
+        CU(cudaEventRecord(ev_halo, st_comm));
+        b.part = 1;
+        go(b);
+        CU(cudaStreamWaitEvent(st, ev_halo, 0));
+        launches += 1;
+      } else {
+        go(s);
+      }
+      fpar ^= 1;
+      vpar ^= 1;
+      return;
+    }
     void* fd = f[1 - fc];
     void* vd = v[1 - vc];
     const void* fsrc = f[fc];
@@ -1125,6 +1216,7 @@ struct lbgpu_engine {
     require_solo();
     if (n <= 0) return;
     const bool want = rp || ra;
+    if (want) require_db("a step residual");
     reset_flags();
     CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long), st));
     if (!fuse_pairs()) {
@@ -1206,6 +1298,7 @@ struct lbgpu_engine {
   void solve(int which, double tol, long long max_iter, long long fixed, int kernel,
              long long* iters, double* resid, int* conv, bool reset_v = true) {
     require_solo();
+    require_db("a solve (its stop rule reads the step residual)");
     const long long n = fixed >= 0 ? fixed : max_iter;
     const char* what = which == 0 ? "iteration" : which == 1 ? "adjoint iteration" : "tangent iteration";
     if (which == 1 && reset_v) {
@@ -1227,6 +1320,8 @@ struct lbgpu_engine {
       const int cur0 = cur;
       long long& steps = which == 0 ? primal_steps : which == 1 ? adjoint_steps : tangent_steps;
       const long long steps0 = steps;
+      // keys of this batch: step k+1 at sweep k (as the captured graphs bake in)
+      (which == 0 ? kb_p : which == 1 ? kb_a : kb_t) = steps0;
       if (fixed < 0 && b > 1) CU(cudaMemcpyAsync(snap, buf[cur], field_bytes(), cudaMemcpyDeviceToDevice, st));
       CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long) * b, st));
       const bool rel = graphs && b == kRing;  // graph batch: step keys 1..kRing
@@ -1248,15 +1343,15 @@ struct lbgpu_engine {
       CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
       CU(cudaMemcpyAsync(h_flags + 4, d_ring, sizeof(unsigned long long) * b, cudaMemcpyDeviceToHost, st));
       sync();
-      // first failing step in the batch, in step order
+      // first failing step in the batch, in step order; the iteration in a
+      // report counts from the start of this solve, as the reference's does
+      // (collision.cpp:387-389)
       long long stop = -1;
       for (long long k = 0; k < b; ++k) {
         const double rk = bits_to_double(h_flags[4 + k]);
         const long long itk = it + k + 1;
-        const long long key_step = rel ? k + 1 : steps0 + k + 1;
-        const bool badk = h_flags[1] != kNoBad && (long long)(h_flags[1] >> 40) == key_step;
-        if (badk)
-          raise_bad(rel ? h_flags[1] + ((unsigned long long)steps0 << 40) : h_flags[1], what);
+        const bool badk = h_flags[1] != kNoBad && (long long)(h_flags[1] >> 40) == k + 1;
+        if (badk) raise_bad(h_flags[1], what, it);
         if (!std::isfinite(rk)) {
           reset_flags();
           if (which == 2)  // adjoint.cpp:472-473
@@ -1286,6 +1381,7 @@ struct lbgpu_engine {
         it += stop + 1;
         break;
       }
+      if (h_flags[1] != kNoBad) raise_bad(h_flags[1], what, it);  // any other bad key
       it += b;
       r = bits_to_double(h_flags[4 + b - 1]);
       batch = std::min<long long>(batch * 2, kRing);
@@ -1301,6 +1397,7 @@ struct lbgpu_engine {
   void tangent(const double* dw_design, double d_inlet_dp, double tol, long long max_iter,
                double* dF, long long* iters, double* resid, int* conv) {
     require_solo();
+    require_db("tangent_solve");
     if (!tg[0]) {
       CU(cudaMalloc(&tg[0], field_bytes()));
       CU(cudaMalloc(&tg[1], field_bytes()));
@@ -1318,7 +1415,7 @@ struct lbgpu_engine {
     CU(cudaMemsetAsync(tg[tc], 0, field_bytes(), st));
     CU(cudaMemsetAsync(tg[1 - tc], 0, field_bytes(), st));
     solve(2, tol, max_iter, -1, 0, iters, resid, conv);
-    const Launch a = launch(tangent_steps);
+    const Launch a = launch(tangent_steps - kb_t);
     if (exact) exact::tangent_terms(a, dim, prec, f[fc], tg[tc], d_support, (long long)support.size(), d_terms);
     else fast::tangent_terms(a, dim, prec, f[fc], tg[tc], d_support, (long long)support.size(), d_terms);
     CU(cudaGetLastError());
@@ -1350,6 +1447,7 @@ struct lbgpu_engine {
   // The engine's primal state, design and model are restored afterwards.
   double fd_gradient(long long ordinal, double h, double tol, long long max_iter, long long fixed) {
     require_solo();
+    require_db("fd_gradient");
     if (ordinal >= (long long)design.size())
       throw Fail{LBGPU_E_ARG, "design ordinal out of range"};
     sync_host_w();
@@ -1389,6 +1487,104 @@ struct lbgpu_engine {
     }
   }
 
+  // fd_gradient for n components with one host sync (fixed >= 0): every side
+  // is queued on the stream -- the raw write of the perturbed value (w and, in
+  // the exact build, its libm pow pair, staged in pinned memory; or rho_in,
+  // which travels with each launch's Model), initialize_state, `fixed`
+  // sweeps, evaluate_raw into a device slot, the write-back. Same sweeps and
+  // reductions as fd_gradient, so the same bits.
+  void fd_batch(long long n, const long long* ords, const double* hs, double tol,
+                long long max_iter, long long fixed, bool from_state, double* out) {
+    require_solo();
+    require_db("fd_gradient");
+    for (long long k = 0; k < n; ++k)
+      if (ords[k] >= (long long)design.size()) throw Fail{LBGPU_E_ARG, "design ordinal out of range"};
+    if (from_state && fixed < 0)
+      throw Fail{LBGPU_E_ARG, "a finite difference from the current state needs fixed_iters >= 0"};
+    if (fixed < 0) {
+      for (long long k = 0; k < n; ++k) out[k] = fd_gradient(ords[k], hs[k], tol, max_iter, -1);
+      return;
+    }
+    sync_host_w();
+    void* save = nullptr;
+    double* stage = nullptr;   // per side: w, p0, p1; then per component: w0, p0, p1
+    double* d_vals = nullptr;  // J of each side
+    const int fc0 = fc;
+    const double rho0 = M.rho_in;
+    auto release = [&] {
+      M.rho_in = rho0;
+      fc = fc0;
+      if (save) cudaMemcpyAsync(f[fc], save, field_bytes(), cudaMemcpyDeviceToDevice, st);
+      cudaStreamSynchronize(st);
+      cudaFree(save), cudaFree(d_vals);
+      if (stage) cudaFreeHost(stage);
+    };
+    try {
+      CU(cudaMalloc(&save, field_bytes()));
+      CU(cudaMemcpyAsync(save, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMallocHost(&stage, sizeof(double) * 9 * std::max<long long>(n, 1)));
+      CU(cudaMalloc(&d_vals, sizeof(double) * 2 * std::max<long long>(n, 1)));
+      auto pows = [&](double val, double* pp) {
+        const double base = M.fluid_power ? val : 1.0 - val;
+        pp[0] = std::pow(base, M.theta), pp[1] = std::pow(base, M.theta - 1.0);
+      };
+      reset_flags();
+      for (long long k = 0; k < n; ++k) {
+        const long long idx = ords[k] >= 0 ? design[ords[k]] : -1;
+        double* sk = stage + 9 * k;
+        for (int side = 0; side < 2; ++side) {
+          const double delta = side == 0 ? hs[k] : -hs[k];
+          if (idx < 0) {
+            M.rho_in = 1.0 + 3.0 * (inlet_dp + delta);  // rho_inlet(), collision.hpp:57
+          } else {
+            double* sv = sk + 3 * side;
+            sv[0] = w[idx] + delta;
+            if (exact) pows(sv[0], sv + 1);
+            CU(cudaMemcpyAsync(d_w + idx, sv, sizeof(double), cudaMemcpyHostToDevice, st));
+            if (exact) {
+              CU(cudaMemcpyAsync(d_p0 + idx, sv + 1, sizeof(double), cudaMemcpyHostToDevice, st));
+              CU(cudaMemcpyAsync(d_p1 + idx, sv + 2, sizeof(double), cudaMemcpyHostToDevice, st));
+            }
+          }
+          if (from_state) {
+            fc = fc0;
+            CU(cudaMemcpyAsync(f[fc], save, field_bytes(), cudaMemcpyDeviceToDevice, st));
+          } else {
+            init_state();
+          }
+          for (long long i = 0; i < fixed; ++i) primal_launch(false, nullptr);
+          const Launch a = launch(primal_steps - kb_p);
+          if (exact) exact::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms, 0);
+          else fast::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms, 0);
+          pairwise_queue(tree_support, d_terms);
+          CU(cudaMemcpyAsync(d_vals + 2 * k + side, d_scalar, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+        if (idx < 0) {
+          M.rho_in = rho0;
+        } else {  // the write-back (fd_gradient's restore)
+          double* s0 = sk + 6;
+          s0[0] = w[idx];
+          if (exact) pows(s0[0], s0 + 1);
+          CU(cudaMemcpyAsync(d_w + idx, s0, sizeof(double), cudaMemcpyHostToDevice, st));
+          if (exact) {
+            CU(cudaMemcpyAsync(d_p0 + idx, s0 + 1, sizeof(double), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(d_p1 + idx, s0 + 2, sizeof(double), cudaMemcpyHostToDevice, st));
+          }
+        }
+      }
+      CU(cudaGetLastError());
+      std::vector<double> vals(size_t(2 * n));
+      CU(cudaMemcpyAsync(vals.data(), d_vals, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+      pull_flags();  // the one host sync
+      if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+      for (long long k = 0; k < n; ++k) out[k] = (vals[2 * k] - vals[2 * k + 1]) / (2.0 * hs[k]);
+    } catch (...) {
+      try { release(); } catch (...) {}
+      throw;
+    }
+    release();
+  }
+
   // ------------------------------------------------------- reductions
   double pairwise(PairTree& tr, const double* d_t) {
     pairwise_queue(tr, d_t);
@@ -1410,10 +1606,11 @@ struct lbgpu_engine {
     launches += 2 + tr.top;
   }
   double objective(const void* buf = nullptr) {
-    const Launch a = launch(primal_steps);
+    const Launch a = launch(primal_steps - kb_p);
     const void* P = buf ? buf : f[fc];
-    if (exact) exact::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms);
-    else fast::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms);
+    const int bm = buf ? 0 : fmode();
+    if (exact) exact::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, bm);
+    else fast::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, bm);
     CU(cudaGetLastError());
     const double val = pairwise(tree_support, d_terms);
     check_bad("iteration");
@@ -1427,16 +1624,17 @@ struct lbgpu_engine {
   }
   void gradient(int kernel, double* g, double* gdp) {
     reset_flags();
-    const Launch a = launch(adjoint_steps);
+    const Launch a = launch(adjoint_steps - kb_a);
     const long long n = (long long)design.size();
-    if (exact) exact::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0);
-    else fast::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0);
+    if (aa && kernel != 0) require_db("the dual-number gradient");
+    if (exact) exact::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0, 0, 0);
+    else fast::gradient(a, dim, prec, kernel, false, f[fc], v[vc], d_design, n, d_grad, nullptr, 0, 0, 0, fmode(), vmode());
     CU(cudaGetLastError());
     if (g && n) CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     if (gdp) {
       const long long ni = (long long)inlets.size();
-      if (exact) exact::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms);
-      else fast::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms);
+      if (exact) exact::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms, 0, 0);
+      else fast::inlet_terms(a, dim, prec, f[fc], v[vc], d_inlets, ni, d_terms, fmode(), vmode());
       CU(cudaGetLastError());
       *gdp = pairwise(tree_inlet, d_terms);
     }
@@ -1473,12 +1671,12 @@ struct lbgpu_engine {
     // mu^n -> grad += g(mu^n, f^{n-1}); mu^{n-1} = adjoint(f^{n-1}, mu^n)
     void back_step(const void* base) {
       const long long nd = (long long)e->design.size();
-      const Launch a = e->launch(e->adjoint_steps);
-      if (e->exact) exact::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1);
-      else fast::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1);
+      const Launch a = e->launch(e->adjoint_steps - e->kb_a);
+      if (e->exact) exact::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
+      else fast::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
       if (!e->inlets.empty()) {
-        if (e->exact) exact::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms);
-        else fast::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms);
+        if (e->exact) exact::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
+        else fast::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
         gdp += e->pairwise(e->tree_inlet, e->d_terms);
       }
       e->M.obj_on = sum ? 1 : 0;
@@ -1526,6 +1724,7 @@ struct lbgpu_engine {
   void unsteady(long long N, bool sum_obj, long long max_slots, double* g, double* gdp, double* J,
                 long long* fsteps) {
     require_solo();
+    require_db("the unsteady adjoint's checkpoint slots");
     if (N < 1) throw Fail{LBGPU_E_ARG, "unsteady adjoint needs at least one step"};
     const long long nslots = std::max<long long>(1, std::min<long long>(max_slots, N));
     std::vector<void*> slots;
@@ -1589,6 +1788,7 @@ struct lbgpu_engine {
                 const double* lambda, long long ri, lbgpu_run_row* rows, long long cap,
                 long long* nrows) {
     require_solo();
+    require_db("the one-shot loop");
     long long k = 0;
     reset_flags();
     const long long n = (long long)design.size();
@@ -1598,9 +1798,9 @@ struct lbgpu_engine {
       primal_launch(rec, nullptr);
       adjoint_launch(0, false, nullptr);
       if (rec) CU(cudaMemsetAsync(d_flags + 2, 0, sizeof(unsigned long long), st));
-      const Launch a = launch(adjoint_steps);
-      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0);
-      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0);
+      const Launch a = launch(adjoint_steps - kb_a);
+      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0, 0, 0);
+      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0, 0, 0);
       CU(cudaGetLastError());
       if (exact) {  // the device moved w: refresh the host copy and the libm pow tables
         CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
@@ -1612,7 +1812,7 @@ struct lbgpu_engine {
         reduce_flags(d_flags + 2, 1, false);
         reduce_flags(d_flags + 1, 1, true);
         pull_flags();
-        if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+        if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration", it0 - 1);
         lbgpu_run_row row;
         row.iteration = double(it);
         row.residual = bits_to_double(h_flags[0]);
@@ -1627,22 +1827,24 @@ struct lbgpu_engine {
       }
     }
     if (!exact) w_host_stale = true;
-    sync();
-    check_bad("iteration");
+    pull_flags();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration", it0 - 1);
     *nrows = k;
   }
 
   // ------------------------------------------------------------ layout
   void to_ref(int field, double* d_out) {
     void* buf = field == 0 ? f[fc] : v[vc];
-    if (exact) exact::layout(G, dim, prec, field, true, buf, d_out, st);
-    else fast::layout(G, dim, prec, field, true, buf, d_out, st);
+    const int fm = field == 0 ? fmode() : vmode();
+    if (exact) exact::layout(G, dim, prec, field, true, buf, d_out, st, 0);
+    else fast::layout(G, dim, prec, field, true, buf, d_out, st, fm);
     CU(cudaGetLastError());
   }
   void from_ref(int field, const double* d_in) {
     void* buf = field == 0 ? f[fc] : v[vc];
-    if (exact) exact::layout(G, dim, prec, field, false, d_in, buf, st);
-    else fast::layout(G, dim, prec, field, false, d_in, buf, st);
+    if (exact) exact::layout(G, dim, prec, field, false, d_in, buf, st, 0);
+    else fast::layout(G, dim, prec, field, false, d_in, buf, st, aa ? 1 : 0);
+    (field == 0 ? fpar : vpar) = 0;  // an in-place field lands in layout O
     CU(cudaGetLastError());
   }
   void ensure_ref() {
@@ -1698,7 +1900,8 @@ int lbgpu_slab_info(const lbgpu_engine* e, int* out6) {
 int lbgpu_group_link(lbgpu_engine** es, int n) {
   if (!es || n < 1) return LBGPU_E_ARG;
   for (int i = 0; i < n; ++i)
-    if (!es[i] || es[i]->slab_count != n || es[i]->slab_id != i || es[i]->device != es[0]->device)
+    if (!es[i] || es[i]->slab_count != n || es[i]->slab_id != i || es[i]->device != es[0]->device ||
+        es[i]->aa)
       return LBGPU_E_ARG;
   if (n == 1) return LBGPU_OK;
   for (int i = 0; i < n; ++i) {
@@ -1725,7 +1928,7 @@ int lbgpu_group_link_p2p(lbgpu_engine** es, int n) {
   if (!es || n < 2) return LBGPU_E_ARG;
   for (int i = 0; i < n; ++i)
     if (!es[i] || es[i]->slab_count != n || es[i]->slab_id != i || !es[i]->ghosts ||
-        es[i]->xmode != 0)
+        es[i]->xmode != 0 || es[i]->aa)
       return LBGPU_E_ARG;
   for (int i = 0; i < n; ++i) {
     lbgpu_engine* e = es[i];
@@ -1886,6 +2089,7 @@ int lbgpu_attach_nccl(lbgpu_engine* e, const void* uid, int nranks, int rank) {
 int lbgpu_exchange(lbgpu_engine* e, int field) {
   if (field != 0 && field != 1) return LBGPU_E_ARG;
   return guarded(e, [&] {
+    e->require_db("a stand-alone halo exchange");
     e->exchange(field);
     e->sync();
   });
@@ -1913,7 +2117,7 @@ int lbgpu_create(const lbgpu_system_desc* desc, lbgpu_engine** out) {
 
 static int desc_from_config(const char* cfg_text, const char* overrides, int device, int exact,
                             CaseSpec& c, SystemArrays& s, lbgpu_system_desc& d,
-                            int slab_count = 1, int slab_id = 0) {
+                            int slab_count = 1, int slab_id = 0, int streaming = 0) {
   std::string err;
   if (!parse_case(cfg_text, overrides ? overrides : "", c, err)) {
     g_create_err = err;
@@ -1939,6 +2143,7 @@ static int desc_from_config(const char* cfg_text, const char* overrides, int dev
   }
   d = lbgpu_system_desc{};
   d.slab_count = slab_count, d.slab_id = slab_id;
+  d.streaming = streaming;
   d.nx = c.nx, d.ny = c.ny, d.nz = c.nz;
   d.precision = c.precision;
   d.exact = exact;
@@ -1977,6 +2182,21 @@ int lbgpu_create_slab_from_config(const char* cfg_text, const char* overrides, i
   SystemArrays s;
   lbgpu_system_desc d;
   const int rc = desc_from_config(cfg_text, overrides, device, exact, c, s, d, slab_count, slab_id);
+  if (rc) return rc;
+  return lbgpu_create(&d, out);
+}
+
+int lbgpu_create_from_config_ex(const char* cfg_text, const char* overrides, int device,
+                                int exact, int slab_count, int slab_id, int streaming,
+                                lbgpu_engine** out) {
+  if (!cfg_text || !out) return LBGPU_E_ARG;
+  *out = nullptr;
+  g_create_err.clear();
+  CaseSpec c;
+  SystemArrays s;
+  lbgpu_system_desc d;
+  const int rc =
+      desc_from_config(cfg_text, overrides, device, exact, c, s, d, slab_count, slab_id, streaming);
   if (rc) return rc;
   return lbgpu_create(&d, out);
 }
@@ -2088,6 +2308,7 @@ int lbgpu_init_state(lbgpu_engine* e) {
 
 int lbgpu_reset_adjoint(lbgpu_engine* e) {
   return guarded(e, [&] {
+    e->vpar = 0;
     CU(cudaMemsetAsync(e->v[e->vc], 0, e->field_bytes(), e->st));
     e->sync();
   });
@@ -2099,7 +2320,9 @@ int lbgpu_upload_state(lbgpu_engine* e, int field, const double* ref) {
     e->ensure_ref();
     CU(cudaMemcpyAsync(e->d_ref, ref, sizeof(double) * e->m * e->N, cudaMemcpyHostToDevice, e->st));
     e->from_ref(field, e->d_ref);
-    if (e->xmode == 2) e->exchange(field);  // ghosts (collective: every rank uploads)
+    // ghosts (collective: every rank uploads); an in-place field lands in
+    // layout O, whose next sweep reads no ghost
+    if (e->xmode == 2 && !e->aa) e->exchange(field);
     e->sync();
   });
 }
@@ -2215,6 +2438,18 @@ int lbgpu_fd_gradient(lbgpu_engine* e, int64_t ordinal, double h, double tol, in
                       int64_t fixed_iters, double* out) {
   if (!out || !(h != 0.0)) return LBGPU_E_ARG;
   return guarded(e, [&] { *out = e->fd_gradient(ordinal, h, tol, max_iter, fixed_iters); });
+}
+
+int lbgpu_fd_gradient_batch(lbgpu_engine* e, int64_t n, const int64_t* ordinals,
+                            const double* steps, double tol, int64_t max_iter,
+                            int64_t fixed_iters, int from_state, double* out) {
+  if (n < 0 || (n > 0 && (!ordinals || !steps || !out))) return LBGPU_E_ARG;
+  for (int64_t k = 0; k < n; ++k)
+    if (!(steps[k] != 0.0)) return LBGPU_E_ARG;
+  return guarded(e, [&] {
+    std::vector<long long> o(ordinals, ordinals + n);
+    e->fd_batch(n, o.data(), steps, tol, max_iter, fixed_iters, from_state != 0, out);
+  });
 }
 
 int lbgpu_pair_steps(lbgpu_engine* e, int64_t n, double* primal_residual,

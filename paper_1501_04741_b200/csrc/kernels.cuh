@@ -100,6 +100,54 @@ __device__ __forceinline__ void gather_async(const R* __restrict__ buf, long lon
   cp_async_commit();
 }
 
+// ---------------------------------------------------------------------
+// Field addressing modes. FM_DB: the double-buffered pull layout (the
+// buffers hold post-collision values; a sweep reads its neighbours' from one
+// buffer and writes its own node in the other). In-place (AA-pattern)
+// streaming keeps ONE buffer per field and alternates two layouts:
+//   FM_O: slot p at node y holds the pre-collision value f_p(y) = post_p(y + D e_p)
+//         (exactly the reference's layout, lattice.hpp:54-100);
+//   FM_E: slot opp(p) at node x holds x's own post-collision value post_p(x).
+// A sweep from O reads and writes its own node only (and leaves E); a sweep
+// from E reads post_p(x + D e_p) at (opp p, x + D e_p) and writes post_q(x)
+// to (q, x - D e_q) (and leaves O). Since e_opp(p) = -e_p, the locations a
+// node writes are exactly the ones it read, so each sweep is in place and
+// race-free, at the same 2 M s bytes per node as the double buffer with half
+// the memory. D = -1 for the primal field, +1 for the adjoint (which streams
+// against the links, adjoint.cpp:239-249).
+enum : int { FM_DB = 0, FM_O = 1, FM_E = 2 };
+template <class L, int D, int FM, int P>
+__device__ __forceinline__ long long in_off(long long N, long long idx, const Nbr& n) {
+  if constexpr (FM == FM_DB) return P * N + nbr_idx<L, P, D>(n);
+  else if constexpr (FM == FM_O) return P * N + idx;
+  else return copp<L>(P) * N + nbr_idx<L, P, D>(n);
+}
+template <class L, int D, int FM, int P>
+__device__ __forceinline__ long long out_off(long long N, long long idx, const Nbr& n) {
+  if constexpr (FM == FM_DB) return P * N + idx;
+  else if constexpr (FM == FM_O) return copp<L>(P) * N + idx;
+  else return P * N + nbr_idx<L, P, -D>(n);
+}
+// gather of the pre-collision populations of node idx under mode FM
+template <class L, class R, int D, int FM>
+__device__ __forceinline__ void gather_m(const R* buf, long long N, long long idx, const Nbr& n,
+                                         R* out) {
+  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(buf + in_off<L, D, FM, P>(N, idx, n)); });
+}
+template <class L, class R, int D, int FM>
+__device__ __forceinline__ void gather_async_m(const R* buf, long long N, long long idx,
+                                               const Nbr& n, R* smem, int stride) {
+  LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, buf + in_off<L, D, FM, P>(N, idx, n)); });
+  cp_async_commit();
+}
+// in-place store of node idx's post-collision values (FM_O / FM_E)
+template <class L, class R, int D, int FM>
+__device__ __forceinline__ void store_aa(R* buf, long long N, long long idx, const Nbr& n,
+                                         const R* v) {
+  static_assert(FM != FM_DB, "double-buffered stores go through store_node");
+  LBGPU_FOR(P, 0, L::M, { buf[out_off<L, D, FM, P>(N, idx, n)] = v[P]; });
+}
+
 // Planes that cross a slab cut for a sweep pulling along D (-1 primal, +1
 // adjoint): side S = -1 are pulled from the left neighbour (D*e_x == -1), S =
 // +1 from the right one; the adjoint's lists are the primal's swapped, the
@@ -219,12 +267,24 @@ __device__ __forceinline__ bool fast_collide(const Model& M, PowPair pp, double 
   node_sums<L, R>(fin, rho, j, T);
   return fast_collide_m<L, R, CK>(M, pp, omt, fin, rho, j[0], j[1], j[2], T, out);
 }
+// The collision given 1/rho (rho > 0 checked by the caller): a fused pair
+// sweep takes the reciprocal once for both halves.
+template <class L, class R, int CK>
+__device__ __forceinline__ void fast_collide_mi(const Model& M, PowPair pp, double omt,
+                                                const R* fin, R rho, R inv, R j0, R j1, R j2,
+                                                R T_, R* out);
 template <class L, class R, int CK>
 __device__ __forceinline__ bool fast_collide_m(const Model& M, PowPair pp, double omt,
                                                const R* fin, R rho, R j0, R j1, R j2, R T_,
                                                R* out) {
   if (!(rho > R(0))) return false;
-  const R inv = R(1) / rho;
+  fast_collide_mi<L, R, CK>(M, pp, omt, fin, rho, R(1) / rho, j0, j1, j2, T_, out);
+  return true;
+}
+template <class L, class R, int CK>
+__device__ __forceinline__ void fast_collide_mi(const Model& M, PowPair pp, double omt,
+                                                const R* fin, R rho, R inv, R j0, R j1, R j2,
+                                                R T_, R* out) {
   const R u[3] = {j0 * inv, j1 * inv, j2 * inv};
   const R G = M.fluid_power ? R(pp.p0) : R(1.0 - pp.p0);
   const R up[3] = {G * u[0], G * u[1], G * u[2]};
@@ -265,7 +325,6 @@ __device__ __forceinline__ bool fast_collide_m(const Model& M, PowPair pp, doubl
     const R geq = R(L::wt(J)) * T * (R(1) + R(3) * eup);
     out[L::MF + J] = g[J] + om * (geq - g[J]);
   });
-  return true;
 }
 
 // Thermal relaxation rate of a node (collision.cpp:210-211).
@@ -298,11 +357,22 @@ __device__ __forceinline__ void flow_sums(const R* f, R& rho, R* j) {
 // The interior VJP reads the base state only through rho, u and T
 // (adjoint.cpp:59, :95): the moment-form entry point takes those.
 template <class L, class R, int CK>
+__device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double omt, R rho,
+                                            R inv, const R* jv, R T, const R* vf, const R* vg,
+                                            R* outf, R* outg);
+template <class L, class R, int CK>
 __device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double omt, R rho,
                                            const R* jv, R T, const R* vf, const R* vg, R* outf,
                                            R* outg) {
   if (!(rho > R(0))) return false;
-  const R inv = R(1) / rho;
+  fast_vjp_mi<L, R, CK>(M, pp, omt, rho, R(1) / rho, jv, T, vf, vg, outf, outg);
+  return true;
+}
+// The VJP given 1/rho (rho > 0 checked by the caller).
+template <class L, class R, int CK>
+__device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double omt, R rho,
+                                            R inv, const R* jv, R T, const R* vf, const R* vg,
+                                            R* outf, R* outg) {
   const R u[3] = {jv[0] * inv, jv[1] * inv, jv[2] * inv};
   const R G = M.fluid_power ? R(pp.p0) : R(1.0 - pp.p0);
   const R up[3] = {G * u[0], G * u[1], G * u[2]};
@@ -383,7 +453,6 @@ __device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double om
   const R om1 = R(1) - om, oms = om * sigma;
 #pragma unroll
   for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k] + oms;
-  return true;
 }
 
 template <class L, class R, int CK>
@@ -543,11 +612,23 @@ __device__ __forceinline__ bool fast_face_vjp(const Model& M, PowPair pp, double
 // shares the interior collision / interior VJP with the other lanes of its
 // warp. The adjoint undoes the reconstruction by hand afterwards
 // (v <- J_recon^T v), again in place, from a handful of scalars.
+// The divisions of the reconstruction are reciprocals of per-model constants
+// (1/rho_target, 1/(1 -+ u_clamp), precomputed on the host) and of the one
+// runtime denominator tden, taken once.
 template <class R>
 struct FaceState {
-  R ua, rho, rho_t, Ksum, Tstar, tden;
+  R ua, rho, Tstar, itden;  // itden = 1 / tden (1 at an inlet)
   bool clamped;
 };
+template <class R>
+__device__ __forceinline__ R face_inv_rho_t(const Model& M, bool inlet) {
+  return R(inlet ? M.inv_rho_in : M.inv_rho_out);
+}
+// 1 / (1 - s ua) for a clamped face (ua = +-u_clamp)
+template <class R>
+__device__ __forceinline__ R face_inv_clamp(const Model& M, R sua) {
+  return R(sua > R(0) ? M.inv_1m_uc : M.inv_1p_uc);
+}
 
 template <class L, class R, int AX, int SG>
 __device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet, double bcT,
@@ -560,14 +641,13 @@ __device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet,
     if constexpr (ea == -SG) km += f[J];
   });
   const R s = R(SG);
-  fs.rho_t = R(inlet ? M.rho_in : M.rho_out);
-  fs.Ksum = k0 + R(2) * km;
-  R ua = s * (R(1) - fs.Ksum / fs.rho_t);
-  R rho = fs.rho_t;
+  const R Ksum = k0 + R(2) * km;
+  R ua = s * (R(1) - Ksum * face_inv_rho_t<R>(M, inlet));
+  R rho = R(inlet ? M.rho_in : M.rho_out);
   fs.clamped = (ua < R(0) ? -ua : ua) > R(M.u_clamp);
   if (fs.clamped) {
     ua = ua > R(0) ? R(M.u_clamp) : R(-M.u_clamp);
-    rho = fs.Ksum / (R(1) - s * ua);
+    rho = Ksum * face_inv_clamp<R>(M, s * ua);
   }
   fs.ua = ua, fs.rho = rho;
   // tangential momentum of the slots parallel to the face (collision.cpp:160-165)
@@ -598,7 +678,7 @@ __device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet,
   R* g = f + L::MF;
   if (inlet) {
     fs.Tstar = R(bcT);
-    fs.tden = R(1);
+    fs.itden = R(1);
   } else {
     R tnum = R(0), tden = R(0);
     LBGPU_FOR(J, 0, L::MT, {
@@ -608,8 +688,8 @@ __device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet,
         tden += R(L::wt(J)) * (R(1) + R(3) * (R(ea) * ua));
       }
     });
-    fs.Tstar = tnum / tden;
-    fs.tden = tden;
+    fs.itden = R(1) / tden;
+    fs.Tstar = tnum * fs.itden;
   }
   LBGPU_FOR(J, 0, L::MT, {
     constexpr int ea = L::et(J, AX);
@@ -621,7 +701,8 @@ __device__ __forceinline__ FaceState<R> face_forward(const Model& M, bool inlet,
 // v <- J_recon^T v for the reconstruction above (the branch the primal value
 // took at the u_clamp test, as the reference's dual sweep does).
 template <class L, class R, int AX, int SG>
-__device__ __forceinline__ void face_reverse(bool inlet, const FaceState<R>& fs, R* v) {
+__device__ __forceinline__ void face_reverse(const Model& M, bool inlet, const FaceState<R>& fs,
+                                             R* v) {
   const R ua = fs.ua, rho = fs.rho, s = R(SG);
   R arho = R(0), aua = R(0), anb[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MF, {
@@ -658,8 +739,8 @@ __device__ __forceinline__ void face_reverse(bool inlet, const FaceState<R>& fs,
 #pragma unroll
     for (int j = 0; j < L::MT; ++j) vg[j] = R(0);
   } else {
-    const R atnum = aT / fs.tden;
-    const R atden = -aT * fs.Tstar / fs.tden;
+    const R atnum = aT * fs.itden;
+    const R atden = -atnum * fs.Tstar;
     LBGPU_FOR(J, 0, L::MT, {
       constexpr int ea = L::et(J, AX);
       if constexpr (ea != SG) {
@@ -670,7 +751,8 @@ __device__ __forceinline__ void face_reverse(bool inlet, const FaceState<R>& fs,
       }
     });
   }
-  const R aK = fs.clamped ? arho / (R(1) - s * ua) : -aua * s / fs.rho_t;
+  const R aK = fs.clamped ? arho * face_inv_clamp<R>(M, s * ua)
+                          : -aua * s * face_inv_rho_t<R>(M, inlet);
   LBGPU_FOR(J, 0, L::MF, {
     constexpr int ea = L::ef(J, AX);
     if constexpr (ea == 0) v[J] += aK;
@@ -695,6 +777,9 @@ __device__ __forceinline__ void face_dispatch(uint8_t code, F&& fn) {
 }  // namespace detail
 using detail::halo_slot;
 using detail::kHaloPlanes;
+using detail::FM_DB;
+using detail::FM_O;
+using detail::FM_E;
 
 namespace detail {
 
@@ -811,21 +896,28 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 // (collision.hpp:103) and, when RESID, the fused step_residual. Pressure-face
 // lanes rebuild their inputs in place (face_forward) and share the interior
 // collision with the rest of the warp.
-template <class L, class R, int CK, bool RESID>
-__device__ __forceinline__ void primal_body(const Launch& a, const R* __restrict__ src,
-                                            R* __restrict__ dst, int x, int y, int z,
-                                            unsigned long long& rmax) {
+// FM: the field's addressing mode (FM_DB: src -> dst; FM_O / FM_E: in place,
+// src == dst, no residual).
+template <class L, class R, int CK, bool RESID, int FM = FM_DB>
+__device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* dst, int x, int y,
+                                            int z, unsigned long long& rmax) {
   using namespace detail;
+  static_assert(FM == FM_DB || !RESID, "in-place sweeps keep no old state for the residual");
   const Geom& g = a.g;
   const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
   const uint8_t code = a.t.code[idx];
   const Nbr nb = make_nbr(g, x, y, z);
   R f[L::M], out[L::M];
-  gather<L, R, -1>(src, g.N, nb, f);
+  if constexpr (FM == FM_DB) gather<L, R, -1>(src, g.N, nb, f);
+  else gather_m<L, R, -1, FM>(src, g.N, idx, nb, f);
   if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
     atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-  store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
-  push_halo<L, R, -1>(a, x, y, z, out);
+  if constexpr (FM == FM_DB) {
+    store_node<L, R, RESID>(src, dst, g.N, idx, f, out, rmax, !is_face(code & TAG_MASK));
+    push_halo<L, R, -1>(a, x, y, z, out);
+  } else {
+    store_aa<L, R, -1, FM>(dst, g.N, idx, nb, out);
+  }
 }
 
 // Plain bounds: ptxas picks 64 regs (FP32) / 96-122 (FP64), no spills. Forcing
@@ -857,6 +949,27 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
+// In-place primal sweep (AA streaming, fast build) from layout FM over the
+// owned columns of the 3-D grid, or, with c0 >= 0, over the slab's two
+// boundary columns c0, c1 only (one thread per (column, y, z); a runtime
+// switch, uniform per launch, to halve the instantiations).
+template <class L, class R, int CK, int FM>
+__global__ void __launch_bounds__(128) k_primal_aa(Launch a, R* A, int c0, int c1) {
+  unsigned long long rmax = 0;
+  if (c0 >= 0) {
+    const long long yz = (long long)a.g.ny * a.g.nz;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < 2 * yz) {
+      const long long r = t % yz;
+      primal_body<L, R, CK, false, FM>(a, A, A, t < yz ? c0 : c1, int(r % a.g.ny),
+                                       int(r / a.g.ny), rmax);
+    }
+  } else {
+    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < a.g.x1) primal_body<L, R, CK, false, FM>(a, A, A, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
+  }
+}
+
 // Adjoint sweep (adjoint_step, adjoint.cpp:206-254, in pull form): gathers v
 // against the links and the frozen base f along them, applies
 // adjoint_collide_node (adjoint.cpp:156-204) and stores the post-collision
@@ -866,11 +979,12 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 // adjoint.cpp:59, :95); face lanes rebuild / un-build in place. SPLIT leaves
 // the rare side-list nodes (synthetic-objective support, support nodes on a
 // face) to k_adjoint_side.
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
+// BM / VM: addressing modes of the base f and of v (in-place v: src == dst).
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM, int BM = FM_DB,
+          int VM = FM_DB>
 __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restrict__ base,
-                                             const R* __restrict__ src, R* __restrict__ dst,
-                                             const R* __restrict__ mom, int x, int y, int z,
-                                             unsigned long long& rmax) {
+                                             const R* src, R* dst, const R* __restrict__ mom,
+                                             int x, int y, int z, unsigned long long& rmax) {
   using namespace detail;
   const Geom& g = a.g;
   const long long N = g.N;
@@ -883,7 +997,8 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
     const Nbr nb = make_nbr(g, x, y, z);
     R vin[L::M], vout[L::M];
     bool ok = true;
-    if (LBGPU_EXACT || AK == 1 || !SPLIT) {
+    if constexpr (LBGPU_EXACT || AK == 1 || !SPLIT) {
+      static_assert(BM == FM_DB && VM == FM_DB, "in-place streaming: product split path only");
       R fin[L::M];
       gather<L, R, -1>(base, N, nb, fin);
       gather<L, R, +1>(src, N, nb, vin);
@@ -895,7 +1010,10 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
       constexpr bool kStage = LBGPU_ADJ_STAGE && sizeof(R) == 8;
       __shared__ R vsm[kStage ? L::M * 128 : 1];
       R* my = vsm + (kStage ? threadIdx.x : 0);
-      if constexpr (kStage) gather_async<L, R, +1>(src, N, nb, my, 128);
+      if constexpr (kStage) {
+        if constexpr (VM == FM_DB) gather_async<L, R, +1>(src, N, nb, my, 128);
+        else gather_async_m<L, R, +1, VM>(src, N, idx, nb, my, 128);
+      }
       R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
       FaceState<R> fs{};
       const bool need = !(tag == TAG_WALL || tag == TAG_HEATER) || (code & CODE_SUPPORT);
@@ -907,14 +1025,13 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         T = mom[(L::DIM + 1) * N + idx];
         if (face) {  // and the face reconstruction's scalars
           const R* fp = mom + (L::DIM + 2) * N + idx;
-          fs.ua = fp[0], fs.rho = fp[N], fs.Tstar = fp[2 * N], fs.tden = fp[3 * N];
+          fs.ua = fp[0], fs.rho = fp[N], fs.Tstar = fp[2 * N], fs.itden = fp[3 * N];
           fs.clamped = fp[4 * N] != R(0);
-          fs.rho_t = R(tag == TAG_INLET ? a.M.rho_in : a.M.rho_out);
-          fs.Ksum = R(0);
         }
       } else if (need) {
         R fin[L::M];
-        gather<L, R, -1>(base, N, nb, fin);
+        if constexpr (BM == FM_DB) gather<L, R, -1>(base, N, nb, fin);
+        else gather_m<L, R, -1, BM>(base, N, idx, nb, fin);
         if (face) {
           const bool inlet = tag == TAG_INLET;
           const double bcT = a.t.bcT[idx];
@@ -929,8 +1046,10 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
       if constexpr (kStage) {
         cp_async_wait_all();
         LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
-      } else {
+      } else if constexpr (VM == FM_DB) {
         gather<L, R, +1>(src, N, nb, vin);
+      } else {
+        gather_m<L, R, +1, VM>(src, N, idx, nb, vin);
       }
       if (tag == TAG_WALL) {
         LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
@@ -947,17 +1066,22 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         if (face) {
           const bool inlet = tag == TAG_INLET;
           face_dispatch<L>(code, [&]<int AX, int SG>() {
-            face_reverse<L, R, AX, SG>(inlet, fs, vout);
+            face_reverse<L, R, AX, SG>(a.M, inlet, fs, vout);
           });
         }
       }
       if (a.M.obj_on && (code & CODE_SUPPORT)) ok = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && ok;
     }
     if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
-    push_halo<L, R, +1>(a, x, y, z, vout);
+    if constexpr (VM == FM_DB) {
+      store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
+      push_halo<L, R, +1>(a, x, y, z, vout);
+    } else {
+      static_assert(!RESID, "in-place sweeps keep no old state for the residual");
+      store_aa<L, R, +1, VM>(dst, N, idx, nb, vout);
+    }
   }
-  }
+}
 
 // Moments of a frozen adjoint base (rho, j, T per node: planes 0..DIM+1),
 // computed once per steady adjoint solve: the moment-form VJP reads the base
@@ -966,7 +1090,7 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
 // arithmetic as the in-sweep path, so the adjoint states are bitwise equal.
 // Pressure-face nodes store the moments of their reconstructed populations
 // and the five scalars face_reverse needs (planes DIM+2 .. DIM+6).
-template <class L, class R>
+template <class L, class R, int BM = FM_DB>
 __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restrict__ base,
                                                       R* __restrict__ mom) {
   using namespace detail;
@@ -982,7 +1106,8 @@ __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restr
   if (!need) return;
   const Nbr nb = make_nbr(g, x, y, z);
   R fin[L::M];
-  gather<L, R, -1>(base, N, nb, fin);
+  if constexpr (BM == FM_DB) gather<L, R, -1>(base, N, nb, fin);
+  else gather_m<L, R, -1, BM>(base, N, idx, nb, fin);
   if (is_face(tag)) {
     FaceState<R> fs;
     const bool inlet = tag == TAG_INLET;
@@ -991,7 +1116,7 @@ __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restr
       fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, fin);
     });
     R* fp = mom + (L::DIM + 2) * N + idx;
-    fp[0] = fs.ua, fp[N] = fs.rho, fp[2 * N] = fs.Tstar, fp[3 * N] = fs.tden;
+    fp[0] = fs.ua, fp[N] = fs.rho, fp[2 * N] = fs.Tstar, fp[3 * N] = fs.itden;
     fp[4 * N] = fs.clamped ? R(1) : R(0);
   }
   R rho, jv[3], T = R(0);
@@ -1060,11 +1185,34 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
-// Side-list adjoint nodes with the full (reference-form) node update.
-template <class L, class R, int CK, bool RESID>
+// In-place adjoint sweep (AA streaming, fast build): base f read under BM, v
+// updated in place from layout VM; COLS as k_primal_aa.
+template <class L, class R, int CK, int BM, int VM, bool MOM>
+__global__ void LBGPU_ADJ_BOUNDS(true, R, MOM) k_adjoint_aa(Launch a, const R* __restrict__ base,
+                                                            R* V, const R* __restrict__ mom,
+                                                            int c0, int c1) {
+  unsigned long long rmax = 0;
+  if (c0 >= 0) {
+    const long long yz = (long long)a.g.ny * a.g.nz;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < 2 * yz) {
+      const long long r = t % yz;
+      adjoint_body<L, R, CK, 0, false, true, MOM, BM, VM>(a, base, V, V, mom, t < yz ? c0 : c1,
+                                                          int(r % a.g.ny), int(r / a.g.ny), rmax);
+    }
+  } else {
+    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < a.g.x1)
+      adjoint_body<L, R, CK, 0, false, true, MOM, BM, VM>(a, base, V, V, mom, x, blockIdx.y,
+                                                          a.g.z0 + blockIdx.z, rmax);
+  }
+}
+
+// Side-list adjoint nodes with the full (reference-form) node update
+// (BM / VM: addressing of base and v, as adjoint_body).
+template <class L, class R, int CK, bool RESID, int BM = FM_DB, int VM = FM_DB>
 __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restrict__ base,
-                                                      const R* __restrict__ src,
-                                                      R* __restrict__ dst,
+                                                      const R* src, R* dst,
                                                       const long long* __restrict__ nodes,
                                                       long long n) {
   using namespace detail;
@@ -1077,37 +1225,52 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
     idx_xyz(g, idx, x, y, z);
     const Nbr nb = make_nbr(g, x, y, z);
     R fin[L::M], vin[L::M], vout[L::M];
-    gather<L, R, -1>(base, g.N, nb, fin);
-    gather<L, R, +1>(src, g.N, nb, vin);
+    if constexpr (BM == FM_DB) gather<L, R, -1>(base, g.N, nb, fin);
+    else gather_m<L, R, -1, BM>(base, g.N, idx, nb, fin);
+    if constexpr (VM == FM_DB) gather<L, R, +1>(src, g.N, nb, vin);
+    else gather_m<L, R, +1, VM>(src, g.N, idx, nb, vin);
     if (!adjoint_node_full<L, R, CK, 0>(a, idx, a.t.code[idx], fin, vin, vout))
       atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
-    store_node<L, R, RESID>(src, dst, g.N, idx, vin, vout, rmax);
-    push_halo<L, R, +1>(a, x, y, z, vout);
+    if constexpr (VM == FM_DB) {
+      store_node<L, R, RESID>(src, dst, g.N, idx, vin, vout, rmax);
+      push_halo<L, R, +1>(a, x, y, z, vout);
+    } else {
+      store_aa<L, R, +1, VM>(dst, g.N, idx, nb, vout);
+    }
   }
   if constexpr (RESID) block_max_bits(rmax, a.fl.resid);
 }
 
-// Experiment knob: stage the f gather through shared memory as well (then
-// 64-thread blocks keep the static shared memory under 48 KB). Measured C3
-// FP64: 5,472 MLUPS per pair against 7,067 with it off.
-#ifndef LBGPU_PAIR_STAGE2
-#define LBGPU_PAIR_STAGE2 0
+// Block shape of the fused pair sweep: BX nodes along x by BY rows of y
+// (one warp per 32 x-nodes). Narrow blocks dilute the pressure-face lanes:
+// a block holding a face node waits on that lane's divergent reconstruction,
+// so with 128-wide rows every block of a 256-column channel pays for it, with
+// 32-wide rows one block in four (measured in DESIGN.md).
+// C3 FP64 (B200, MLUPS per pair): 128x1 7,433; 64x1 7,529; 32x1 7,443;
+// 32x4 7,689 -- the last equals the face-free periodic box (7,696).
+#ifndef LBGPU_PAIR_BX
+#define LBGPU_PAIR_BX 32
+#endif
+#ifndef LBGPU_PAIR_BY
+#define LBGPU_PAIR_BY 4
 #endif
 template <class R>
-constexpr int kPairThreads = (LBGPU_PAIR_STAGE2 && sizeof(R) == 8) ? 64 : 128;
+constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 
 // Fused primal + adjoint pair (product build): adjoint sweep n (base
 // f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
-// gathers it once, takes its moments once (node_sums), collides it
-// (primal_node's fast path) and runs the moment-form VJP against it
-// (adjoint_body's split path): 4 M s bytes per node for the pair instead of
-// 5 M s. Each half is bitwise the stand-alone sweep (same functions, same
-// operands). Side-list nodes' adjoint half goes to k_adjoint_side as usual.
-template <class L, class R, int CK, bool RESID>
-__device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__ fsrc,
-                                          R* __restrict__ fdst, const R* __restrict__ vsrc,
-                                          R* __restrict__ vdst, int x, int y, int z,
+// gathers it once, takes its moments once (node_sums) and the node's
+// switching pair, thermal rate and 1/rho once, collides it (primal_node's
+// fast path) and runs the moment-form VJP against it (adjoint_body's split
+// path): 4 M s bytes per node for the pair instead of 5 M s. Each half is
+// bitwise the stand-alone sweep (same functions, same operands). Side-list
+// nodes' adjoint half goes to k_adjoint_side as usual.
+// FM / VM: addressing of f and v (in place: fsrc == fdst, vsrc == vdst).
+template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB>
+__device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fdst,
+                                          const R* vsrc, R* vdst, int x, int y, int z, int tid,
                                           unsigned long long& rP, unsigned long long& rA) {
+  static_assert((FM == FM_DB && VM == FM_DB) || !RESID, "in-place sweeps: no residual");
   using namespace detail;
   const Geom& g = a.g;
   const long long N = g.N;
@@ -1115,33 +1278,35 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
   const uint8_t code = a.t.code[idx];
   const int tag = code & TAG_MASK;
   const bool face = is_face(tag);
+  const bool bb = tag == TAG_WALL || tag == TAG_HEATER;  // bounce-back: no collision
   const bool side = (code & CODE_SUPPORT) && (a.M.obj_kind == 2 || face);
   const Nbr nb = make_nbr(g, x, y, z);
   constexpr bool kStage = LBGPU_ADJ_STAGE && sizeof(R) == 8;
-  constexpr bool kStage2 = LBGPU_PAIR_STAGE2 && sizeof(R) == 8;  // f staged too
   constexpr int kTB = kPairThreads<R>;
-  __shared__ R fsm[kStage2 ? L::M * kTB : 1];
   __shared__ R vsm[kStage ? L::M * kTB : 1];
-  R* myf = fsm + (kStage2 ? threadIdx.x : 0);
-  R* my = vsm + (kStage ? threadIdx.x : 0);
-  if constexpr (kStage2) gather_async<L, R, -1>(fsrc, N, nb, myf, kTB);
-  if constexpr (kStage)
-    if (!side) gather_async<L, R, +1>(vsrc, N, nb, my, kTB);
-  R rho = R(1), jv[3] = {R(0), R(0), R(0)}, T = R(0);
+  R* my = vsm + (kStage ? tid : 0);
+  if constexpr (kStage) {
+    if constexpr (VM == FM_DB) {
+      if (!side) gather_async<L, R, +1>(vsrc, N, nb, my, kTB);
+    } else {
+      if (!side) gather_async_m<L, R, +1, VM>(vsrc, N, idx, nb, my, kTB);
+    }
+  }
+  // the node's constants, shared by both halves
+  double w = 1.0, omt = 0.0;
+  PowPair pp{};
+  if (!bb) {
+    w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+    pp = node_pp<false>(a.M, a.t, idx, code, w);
+    omt = node_omt<R>(a.M, a.t, code, w);
+  }
+  R rho, jv[3], T, inv = R(1);
   FaceState<R> fs{};
   bool okP = true, okA = true;
   {
     R f[L::M], out[L::M];
-    if constexpr (kStage2) {
-      if (!side) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      else cp_async_wait_all();
-      LBGPU_FOR(P, 0, L::M, { f[P] = myf[P * kTB]; });
-    } else {
-      gather<L, R, -1>(fsrc, N, nb, f);
-    }
-    double w = 1.0;
-    PowPair pp{};
-    double omt = 0.0;
+    if constexpr (FM == FM_DB) gather<L, R, -1>(fsrc, N, nb, f);
+    else gather_m<L, R, -1, FM>(fsrc, N, idx, nb, f);
     if (tag == TAG_WALL) {
       LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
     } else if (tag == TAG_HEATER) {
@@ -1149,31 +1314,35 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
       const R Th = R(a.t.bcT[idx]);
 #pragma unroll
       for (int j = 0; j < L::MT; ++j) out[L::MF + j] = R(L::wt(j)) * Th * (R(1) + R(3) * R(0));
-    } else {
-      w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-      pp = node_pp<false>(a.M, a.t, idx, code, w);
-      omt = node_omt<R>(a.M, a.t, code, w);
-      if (face) {
-        const bool inlet = tag == TAG_INLET;
-        const double bcT = a.t.bcT[idx];
-        face_dispatch<L>(code, [&]<int AX, int SG>() {
-          fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, f);
-        });
-      }
+    } else if (face) {
+      const bool inlet = tag == TAG_INLET;
+      const double bcT = a.t.bcT[idx];
+      face_dispatch<L>(code, [&]<int AX, int SG>() {
+        fs = face_forward<L, R, AX, SG>(a.M, inlet, bcT, f);
+      });
     }
     node_sums<L, R>(f, rho, jv, T);
-    if (!(tag == TAG_WALL || tag == TAG_HEATER))
-      okP = fast_collide_m<L, R, CK>(a.M, pp, omt, f, rho, jv[0], jv[1], jv[2], T, out);
-    store_node<L, R, RESID>(fsrc, fdst, N, idx, f, out, rP, !face);
-    push_halo<L, R, -1>(a, x, y, z, out);
+    if (rho > R(0)) inv = R(1) / rho;
+    if (!bb) {
+      if (rho > R(0)) fast_collide_mi<L, R, CK>(a.M, pp, omt, f, rho, inv, jv[0], jv[1], jv[2], T, out);
+      else okP = false;
+    }
+    if constexpr (FM == FM_DB) {
+      store_node<L, R, RESID>(fsrc, fdst, N, idx, f, out, rP, !face);
+      push_halo<L, R, -1>(a, x, y, z, out);
+    } else {
+      store_aa<L, R, -1, FM>(fdst, N, idx, nb, out);
+    }
   }
   if (!side) {
     R vin[L::M], vout[L::M];
     if constexpr (kStage) {
       cp_async_wait_all();
       LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * kTB]; });
-    } else {
+    } else if constexpr (VM == FM_DB) {
       gather<L, R, +1>(vsrc, N, nb, vin);
+    } else {
+      gather_m<L, R, +1, VM>(vsrc, N, idx, nb, vin);
     }
     if (tag == TAG_WALL) {
       LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
@@ -1182,20 +1351,24 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
 #pragma unroll
       for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
     } else {
-      const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-      const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
-      const double omt = node_omt<R>(a.M, a.t, code, w);
-      okA = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout, vout + L::MF);
+      if (rho > R(0))
+        fast_vjp_mi<L, R, CK>(a.M, pp, omt, rho, inv, jv, T, vin, vin + L::MF, vout, vout + L::MF);
+      else
+        okA = false;
       if (face) {
         const bool inlet = tag == TAG_INLET;
         face_dispatch<L>(code, [&]<int AX, int SG>() {
-          face_reverse<L, R, AX, SG>(inlet, fs, vout);
+          face_reverse<L, R, AX, SG>(a.M, inlet, fs, vout);
         });
       }
     }
     if (a.M.obj_on && (code & CODE_SUPPORT)) okA = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && okA;
-    store_node<L, R, RESID>(vsrc, vdst, N, idx, vin, vout, rA);
-    push_halo<L, R, +1>(a, x, y, z, vout);
+    if constexpr (VM == FM_DB) {
+      store_node<L, R, RESID>(vsrc, vdst, N, idx, vin, vout, rA);
+      push_halo<L, R, +1>(a, x, y, z, vout);
+    } else {
+      store_aa<L, R, +1, VM>(vdst, N, idx, nb, vout);
+    }
   }
   if (!(okP && okA)) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
 }
@@ -1206,23 +1379,26 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* __restrict__
 #ifndef LBGPU_PAIR_MINB32
 #define LBGPU_PAIR_MINB32 5
 #endif
-// FP64 pair, C3 MLUPS: 3 blocks (168 regs) 6,711; 4 (128 regs) 7,067; 5 (96
-// regs + 248 B spill) 5,381.
+// FP64 pair, C3 MLUPS (128-thread blocks): 3 blocks (168 regs) 6,711; 4 (128
+// regs) 7,067; 5 (96 regs + 248 B spill) 5,381. The bound is kept per 128
+// threads whatever the block shape.
 #ifndef LBGPU_PAIR_MINB
 #define LBGPU_PAIR_MINB LBGPU_ADJ_MINB
 #endif
 #define LBGPU_PAIR_BOUNDS(R)                                                   \
   __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_PAIR_MINB) * \
-                                         (128 / kPairThreads<R>))
+                                         128 / kPairThreads<R>)
 template <class L, class R, int CK, bool RESID>
 __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
                                                         R* __restrict__ fdst,
                                                         const R* __restrict__ vsrc,
                                                         R* __restrict__ vdst) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
   unsigned long long rP = 0, rA = 0;
-  if (x < a.g.x1)
-    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, x, blockIdx.y, a.g.z0 + blockIdx.z, rP, rA);
+  if (x < a.g.x1 && y < a.g.ny)
+    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, x, y, a.g.z0 + blockIdx.z,
+                               threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
   if constexpr (RESID) {
     detail::block_max_bits(rP, a.fl.resid);
     detail::block_max_bits(rA, a.fl.aux);
@@ -1240,11 +1416,35 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair_cols(Launch a, const R* __restrict__
   if (t < 2 * yz) {
     const long long r = t % yz;
     pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, t < yz ? c0 : c1, int(r % a.g.ny),
-                               int(r / a.g.ny), rP, rA);
+                               int(r / a.g.ny), threadIdx.x, rP, rA);
   }
   if constexpr (RESID) {
     detail::block_max_bits(rP, a.fl.resid);
     detail::block_max_bits(rA, a.fl.aux);
+  }
+}
+
+// In-place fused pair (AA streaming): f from layout FM, v from layout VM,
+// each updated in place; COLS as k_primal_aa. The side-list adjoint nodes run
+// BEFORE it (k_adjoint_side reads the base f^{n+1} that this kernel
+// overwrites; their v locations are theirs alone).
+template <class L, class R, int CK, int FM, int VM>
+__global__ void LBGPU_PAIR_BOUNDS(R) k_pair_aa(Launch a, R* F, R* V, int c0, int c1) {
+  unsigned long long rP = 0, rA = 0;
+  if (c0 >= 0) {
+    const long long yz = (long long)a.g.ny * a.g.nz;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < 2 * yz) {
+      const long long r = t % yz;
+      pair_body<L, R, CK, false, FM, VM>(a, F, F, V, V, t < yz ? c0 : c1, int(r % a.g.ny),
+                                         int(r / a.g.ny), threadIdx.x, rP, rA);
+    }
+  } else {
+    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x < a.g.x1 && y < a.g.ny)
+      pair_body<L, R, CK, false, FM, VM>(a, F, F, V, V, x, y, a.g.z0 + blockIdx.z,
+                                         threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
   }
 }
 
@@ -1256,7 +1456,7 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair_cols(Launch a, const R* __restrict__
 // — so it carries no dual-number code; design nodes on any other tag (none
 // for config-built cases, config.cpp:355) are the SIDE launch over
 // NodeTables::grad_side with the dual path (design_gradient_node_dual).
-template <class L, class R, int AK, bool UPDATE, bool SIDE>
+template <class L, class R, int AK, bool UPDATE, bool SIDE, int BM = FM_DB, int VM = FM_DB>
 __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict__ p,
                                                   const R* __restrict__ q,
                                                   const long long* __restrict__ nodes,
@@ -1279,8 +1479,8 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
       const int z = int(idx / ((long long)g.nx * g.ny));
       const Nbr nb = make_nbr(g, x, y, z);
       R f[L::M], v[L::M];
-      gather<L, R, -1>(p, g.N, nb, f);
-      gather<L, R, +1>(q, g.N, nb, v);
+      gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
+      gather_m<L, R, +1, VM>(q, g.N, idx, nb, v);
       const double w = a.t.w[idx];
       const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
       double gv = 0.0;
@@ -1379,7 +1579,7 @@ __global__ void k_tangent_terms(Launch a, const R* __restrict__ base, const R* _
 }
 
 // Objective terms F^x on the support list (evaluate_raw, objective.cpp:64-72).
-template <class L, class R>
+template <class L, class R, int BM = FM_DB>
 __global__ void k_objective_terms(Launch a, const R* __restrict__ p,
                                   const long long* __restrict__ nodes, long long n,
                                   double* __restrict__ terms) {
@@ -1391,7 +1591,7 @@ __global__ void k_objective_terms(Launch a, const R* __restrict__ p,
   const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
   const Nbr nb = make_nbr(g, x, y, z);
   R f[L::M];
-  gather<L, R, -1>(p, g.N, nb, f);
+  gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
   R t;
   if (!node_term<L, R>(a.M, f, t)) {
     atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
@@ -1402,7 +1602,7 @@ __global__ void k_objective_terms(Launch a, const R* __restrict__ p,
 
 // Inlet-overpressure global (param_gradient, adjoint.cpp:399-418): one dual
 // collision per inlet node with rho_target seeded by 3.
-template <class L, class R>
+template <class L, class R, int BM = FM_DB, int VM = FM_DB>
 __global__ void k_inlet_terms(Launch a, const R* __restrict__ p, const R* __restrict__ q,
                               const long long* __restrict__ nodes, long long n,
                               double* __restrict__ terms) {
@@ -1414,8 +1614,8 @@ __global__ void k_inlet_terms(Launch a, const R* __restrict__ p, const R* __rest
   const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
   const Nbr nb = make_nbr(g, x, y, z);
   R f[L::M], v[L::M];
-  gather<L, R, -1>(p, g.N, nb, f);
-  gather<L, R, +1>(q, g.N, nb, v);
+  gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
+  gather_m<L, R, +1, VM>(q, g.N, idx, nb, v);
   const uint8_t code = a.t.code[idx];
   const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
   const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code, w);
@@ -1435,7 +1635,9 @@ __global__ void k_inlet_terms(Launch a, const R* __restrict__ p, const R* __rest
 // Reference-layout conversion. D = -1: primal (f_ref(x) = post(x - e)),
 // D = +1: adjoint (v_ref(x) = post(x + e)). TO_REF gathers post -> ref,
 // otherwise scatters ref -> post (the exact inverse permutation).
-template <class L, class R, int D, bool TO_REF>
+// FM: the post buffer's addressing mode; an in-place field is always
+// uploaded into layout O (where it equals the reference layout).
+template <class L, class R, int D, bool TO_REF, int FM = FM_DB>
 __global__ void k_layout(Geom g, const void* __restrict__ in, void* __restrict__ out) {
   using namespace detail;
   const int x = g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -1447,12 +1649,17 @@ __global__ void k_layout(Geom g, const void* __restrict__ in, void* __restrict__
   if constexpr (TO_REF) {
     const R* post = static_cast<const R*>(in);
     double* ref = static_cast<double*>(out);
-    LBGPU_FOR(P, 0, L::M, { ref[P * N + idx] = double(post[P * N + nbr_idx<L, P, D>(nb)]); });
+    LBGPU_FOR(P, 0, L::M, { ref[P * N + idx] = double(post[in_off<L, D, FM, P>(N, idx, nb)]); });
   } else {
     const double* ref = static_cast<const double*>(in);
     R* post = static_cast<R*>(out);
-    // post(y) = ref(y - D e)
-    LBGPU_FOR(P, 0, L::M, { post[P * N + idx] = R(ref[P * N + nbr_idx<L, P, -D>(nb)]); });
+    if constexpr (FM == FM_DB) {
+      // post(y) = ref(y - D e)
+      LBGPU_FOR(P, 0, L::M, { post[P * N + idx] = R(ref[P * N + nbr_idx<L, P, -D>(nb)]); });
+    } else {
+      static_assert(FM == FM_O, "uploads land in layout O");
+      LBGPU_FOR(P, 0, L::M, { post[P * N + idx] = R(ref[P * N + idx]); });
+    }
   }
 }
 
@@ -1523,6 +1730,43 @@ __global__ void k_halo_pull(Geom g, R* __restrict__ buf, const R* __restrict__ l
     buf[pr * g.N + (long long)g.nx * t + (g.nx - 1)] =
         left[pr * gl.N + (long long)gl.nx * t + (gl.x1 - 1)];
     buf[pl * g.N + (long long)g.nx * t + g.x1] = right[pl * gr.N + (long long)gr.nx * t + gr.x0];
+  }
+}
+
+// In-place (AA) streaming across slab cuts. A sweep from layout E writes the
+// slots that cross a cut into the ghost columns (node x0 stores to x0 - D e_q
+// for D e_x(q) = +1, i.e. the left ghost; x1-1 to the right ghost for
+// D e_x(q) = -1); they belong to the neighbours' boundary columns, in layout
+// O. The reverse exchange ships them there: pack from the ghosts, unpack
+// into the receiver's owned boundary columns. (A sweep from O reads its own
+// node only; its E-layout boundary values reach the neighbours' ghosts by
+// the forward exchange, k_halo_pack / k_halo_unpack with D negated.)
+template <class L, class R, int D>
+__global__ void k_halo_rpack(Geom g, const R* __restrict__ buf, R* __restrict__ send_left,
+                             R* __restrict__ send_right) {
+  const long long yz = (long long)g.ny * g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= yz) return;
+  const long long row = (long long)g.nx * t;
+#pragma unroll
+  for (int k = 0; k < kHaloPlanes<L>; ++k) {
+    const int pl = halo_slot<L, D, +1>(k), pr = halo_slot<L, D, -1>(k);
+    send_left[k * yz + t] = buf[pl * g.N + row + (g.nx - 1)];  // left ghost
+    send_right[k * yz + t] = buf[pr * g.N + row + g.x1];      // right ghost
+  }
+}
+template <class L, class R, int D>
+__global__ void k_halo_runpack(Geom g, R* __restrict__ buf, const R* __restrict__ recv_left,
+                               const R* __restrict__ recv_right) {
+  const long long yz = (long long)g.ny * g.nz;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= yz) return;
+  const long long row = (long long)g.nx * t;
+#pragma unroll
+  for (int k = 0; k < kHaloPlanes<L>; ++k) {
+    const int pr = halo_slot<L, D, -1>(k), pl = halo_slot<L, D, +1>(k);
+    buf[pr * g.N + row + g.x0] = recv_left[k * yz + t];        // the left neighbour's right ghost
+    buf[pl * g.N + row + (g.x1 - 1)] = recv_right[k * yz + t]; // the right neighbour's left ghost
   }
 }
 
@@ -1616,6 +1860,20 @@ void adjoint_l(const SweepArgs& s, const void* base, const void* src, void* dst)
   }
 }
 
+// addressing mode (0 FM_DB, 1 FM_O, 2 FM_E) -> compile-time NAME
+#define LBGPU_FM_DISPATCH(MODE, NAME, ...)                              \
+  do {                                                                  \
+    if ((MODE) == FM_DB) { constexpr int NAME = FM_DB; __VA_ARGS__; }   \
+    else if ((MODE) == FM_O) { constexpr int NAME = FM_O; __VA_ARGS__; } \
+    else { constexpr int NAME = FM_E; __VA_ARGS__; }                    \
+  } while (0)
+// in-place layouts only (FM_O, FM_E)
+#define LBGPU_AA_DISPATCH(MODE, NAME, ...)                              \
+  do {                                                                  \
+    if ((MODE) == FM_O) { constexpr int NAME = FM_O; __VA_ARGS__; }     \
+    else { constexpr int NAME = FM_E; __VA_ARGS__; }                    \
+  } while (0)
+
 #define LBGPU_LR_DISPATCH(DIM, PREC, ...)                                   \
   do {                                                                      \
     if ((DIM) == 2 && (PREC) == 64) { using L = LatD2; using R = double; __VA_ARGS__; } \
@@ -1633,6 +1891,8 @@ void primal(const SweepArgs& s, const void* src, void* dst) {
 void adjoint(const SweepArgs& s, const void* base, const void* src, void* dst) {
   LBGPU_LR_DISPATCH(s.dim, s.prec, (adjoint_l<L, R, 0>(s, base, src, dst)));
 }
+#endif
+#if defined(LBGPU_PART_PAIR)
 // k_pair over s.part's columns, then the side-list adjoint nodes (part != 1);
 // the primal residual goes to a.fl.resid, the adjoint's to a.fl.aux.
 template <class L, class R, int CK, bool RES>
@@ -1650,9 +1910,13 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
   } else {
     if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
     if (a.g.x1 > a.g.x0) {
-      const int bx = (a.g.x1 - a.g.x0) >= TB ? TB : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-      dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
-      k_pair<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
+      const int wx = a.g.x1 - a.g.x0;
+      const int bx = wx >= LBGPU_PAIR_BX ? LBGPU_PAIR_BX : (wx >= 64 ? 64 : 32);
+      const int by = TB / bx;  // narrow slabs: more rows per block
+      int nzs = a.g.nz;
+      if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (design pair)
+      dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, nzs);
+      k_pair<L, R, CK, RES><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
     }
   }
   if (s.n_adj_side > 0 && s.part != 1) {
@@ -1672,11 +1936,119 @@ void pair(const SweepArgs& s, const void* fsrc, void* fdst, const void* vsrc, vo
   });
 #endif
 }
-void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom) {
+#endif
+#if defined(LBGPU_PART_ADJOINT)
+void base_moments(const Launch& a, int dim, int prec, int bm, const void* base, void* mom) {
   const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
   dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz);
-  LBGPU_LR_DISPATCH(dim, prec, (k_base_moments<L, R><<<grid, bx, 0, a.stream>>>(
-                                    a, static_cast<const R*>(base), static_cast<R*>(mom))));
+  LBGPU_LR_DISPATCH(dim, prec, LBGPU_FM_DISPATCH(bm, BM, (k_base_moments<L, R, BM><<<grid, bx, 0, a.stream>>>(
+                                    a, static_cast<const R*>(base), static_cast<R*>(mom)))));
+}
+#endif
+#if defined(LBGPU_PART_AA)
+// In-place (AA) sweeps, product build: s.fm / s.vm are the current layouts
+// (FM_O / FM_E) of f and v; s.part as for the double-buffered launchers.
+// launch(a, grid, block, c0, c1): c0 >= 0 selects the boundary-column mode
+template <class F>
+static void aa_grid(const SweepArgs& s, F&& launch) {
+  Launch a = s.a;
+  if (s.part == 2) {
+    const long long n = 2ll * a.g.ny * a.g.nz;
+    launch(a, dim3(unsigned((n + 127) / 128)), dim3(128), a.g.x0, a.g.x1 - 1);
+    return;
+  }
+  if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+  if (a.g.x1 <= a.g.x0) return;
+  const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+  launch(a, dim3((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz), dim3(bx), -1, -1);
+}
+void primal_aa(const SweepArgs& s, void* A) {
+#if !LBGPU_EXACT
+  LBGPU_LR_DISPATCH(s.dim, s.prec, LBGPU_CK_DISPATCH(LBGPU_AA_DISPATCH(s.fm, FM, {
+    aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
+      k_primal_aa<L, R, CKV, FM><<<grid, block, 0, a.stream>>>(a, static_cast<R*>(A), c0, c1);
+    });
+  })));
+#else
+  (void)s, (void)A;
+#endif
+}
+void adjoint_aa(const SweepArgs& s, const void* base, void* V) {
+#if !LBGPU_EXACT
+  const bool mom = s.mom != nullptr;
+  LBGPU_LR_DISPATCH(s.dim, s.prec, LBGPU_CK_DISPATCH(LBGPU_AA_DISPATCH(s.vm, VM, {
+    {
+      const R* b = static_cast<const R*>(base);
+      const R* mo = static_cast<const R*>(s.mom);
+      R* v = static_cast<R*>(V);
+      if (mom) {  // frozen base: its moments (any base layout)
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
+          k_adjoint_aa<L, R, CKV, FM_O, VM, true><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        });
+      } else if (s.fm == FM_O) {
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
+          k_adjoint_aa<L, R, CKV, FM_O, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        });
+      } else {
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
+          k_adjoint_aa<L, R, CKV, FM_E, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        });
+      }
+      if (s.n_adj_side > 0 && s.part != 1) {
+        const unsigned nb = unsigned((s.n_adj_side + 127) / 128);
+        if (s.fm == FM_O)
+          k_adjoint_side<L, R, CKV, false, FM_O, VM><<<nb, 128, 0, s.a.stream>>>(s.a, b, v, v, s.adj_side, s.n_adj_side);
+        else
+          k_adjoint_side<L, R, CKV, false, FM_E, VM><<<nb, 128, 0, s.a.stream>>>(s.a, b, v, v, s.adj_side, s.n_adj_side);
+      }
+    }
+  })));
+#else
+  (void)s, (void)base, (void)V;
+#endif
+}
+#endif
+#if defined(LBGPU_PART_AAPAIR)
+void pair_aa(const SweepArgs& s, void* F, void* V) {
+#if !LBGPU_EXACT
+  LBGPU_LR_DISPATCH(s.dim, s.prec, LBGPU_CK_DISPATCH({
+    R* f = static_cast<R*>(F);
+    R* v = static_cast<R*>(V);
+    // side-list adjoint nodes first: they read the base this kernel overwrites
+    if (s.n_adj_side > 0 && s.part != 1) {
+      const unsigned nb = unsigned((s.n_adj_side + 127) / 128);
+      auto side = [&]<int FM, int VM>() {
+        k_adjoint_side<L, R, CKV, false, FM, VM><<<nb, 128, 0, s.a.stream>>>(s.a, f, v, v, s.adj_side, s.n_adj_side);
+      };
+      if (s.fm == FM_O && s.vm == FM_O) side.template operator()<FM_O, FM_O>();
+      else if (s.fm == FM_O) side.template operator()<FM_O, FM_E>();
+      else if (s.vm == FM_O) side.template operator()<FM_E, FM_O>();
+      else side.template operator()<FM_E, FM_E>();
+    }
+    auto go = [&]<int FM, int VM>() {
+      Launch a = s.a;
+      constexpr int TB = kPairThreads<R>;
+      if (s.part == 2) {
+        const long long n = 2ll * a.g.ny * a.g.nz;
+        k_pair_aa<L, R, CKV, FM, VM><<<unsigned((n + TB - 1) / TB), TB, 0, a.stream>>>(a, f, v, a.g.x0, a.g.x1 - 1);
+        return;
+      }
+      if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+      if (a.g.x1 <= a.g.x0) return;
+      const int wx = a.g.x1 - a.g.x0;
+      const int bx = wx >= LBGPU_PAIR_BX ? LBGPU_PAIR_BX : (wx >= 64 ? 64 : 32);
+      const int by = TB / bx;
+      dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, a.g.nz);
+      k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v, -1, -1);
+    };
+    if (s.fm == FM_O && s.vm == FM_O) go.template operator()<FM_O, FM_O>();
+    else if (s.fm == FM_O) go.template operator()<FM_O, FM_E>();
+    else if (s.vm == FM_O) go.template operator()<FM_E, FM_O>();
+    else go.template operator()<FM_E, FM_E>();
+  }));
+#else
+  (void)s, (void)F, (void)V;
+#endif
 }
 #endif
 #if defined(LBGPU_PART_ADJDUAL)
@@ -1687,7 +2059,7 @@ void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* d
 #if defined(LBGPU_PART_AUX)
 void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,
               const void* q, const long long* nodes, long long n, double* gout, double* w_rw,
-              double zeta, double lambda, int accumulate) {
+              double zeta, double lambda, int accumulate, int bm, int vm) {
   if (n <= 0) return;
   const int bs = 128;
   const unsigned nb = unsigned((n + bs - 1) / bs);
@@ -1695,7 +2067,22 @@ void gradient(const Launch& a, int dim, int prec, int ak, bool update, const voi
     const R* pp = static_cast<const R*>(p);
     const R* qq = static_cast<const R*>(q);
     const unsigned ns = unsigned((a.t.n_grad_side + bs - 1) / bs);
-    if (ak == 0 && !update) {
+    if (bm != FM_DB || vm != FM_DB) {  // in-place fields: param_gradient only
+#if !LBGPU_EXACT
+      auto go = [&]<int BM, int VM>() {
+        if (ak == 0) {
+          k_gradient<L, R, 0, false, false, BM, VM><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+          if (ns) k_gradient<L, R, 1, false, true, BM, VM><<<ns, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+        } else {
+          k_gradient<L, R, 1, false, false, BM, VM><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
+        }
+      };
+      if (bm == FM_O && vm == FM_O) go.template operator()<FM_O, FM_O>();
+      else if (bm == FM_O) go.template operator()<FM_O, FM_E>();
+      else if (vm == FM_O) go.template operator()<FM_E, FM_O>();
+      else go.template operator()<FM_E, FM_E>();
+#endif
+    } else if (ak == 0 && !update) {
       k_gradient<L, R, 0, false, false><<<nb, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
       if (ns) k_gradient<L, R, 1, false, true><<<ns, bs, 0, a.stream>>>(a, pp, qq, nodes, n, gout, w_rw, zeta, lambda, accumulate);
     } else if (ak == 0) {
@@ -1709,19 +2096,25 @@ void gradient(const Launch& a, int dim, int prec, int ak, bool update, const voi
   });
 }
 void objective_terms(const Launch& a, int dim, int prec, const void* p, const long long* nodes,
-                     long long n, double* terms) {
+                     long long n, double* terms, int bm) {
   if (n <= 0) return;
   const unsigned nb = unsigned((n + 127) / 128);
-  LBGPU_LR_DISPATCH(dim, prec, (k_objective_terms<L, R><<<nb, 128, 0, a.stream>>>(
-                                    a, static_cast<const R*>(p), nodes, n, terms)));
+  LBGPU_LR_DISPATCH(dim, prec, LBGPU_FM_DISPATCH(bm, BM, (k_objective_terms<L, R, BM><<<nb, 128, 0, a.stream>>>(
+                                    a, static_cast<const R*>(p), nodes, n, terms))));
 }
 void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,
-                 const long long* nodes, long long n, double* terms) {
+                 const long long* nodes, long long n, double* terms, int bm, int vm) {
   if (n <= 0) return;
   const unsigned nb = unsigned((n + 127) / 128);
-  LBGPU_LR_DISPATCH(dim, prec, (k_inlet_terms<L, R><<<nb, 128, 0, a.stream>>>(
-                                    a, static_cast<const R*>(p), static_cast<const R*>(q),
-                                    nodes, n, terms)));
+  LBGPU_LR_DISPATCH(dim, prec, {
+    const R* pp = static_cast<const R*>(p);
+    const R* qq = static_cast<const R*>(q);
+    if (bm == FM_DB && vm == FM_DB) k_inlet_terms<L, R><<<nb, 128, 0, a.stream>>>(a, pp, qq, nodes, n, terms);
+    else if (bm == FM_O && vm == FM_O) k_inlet_terms<L, R, FM_O, FM_O><<<nb, 128, 0, a.stream>>>(a, pp, qq, nodes, n, terms);
+    else if (bm == FM_O) k_inlet_terms<L, R, FM_O, FM_E><<<nb, 128, 0, a.stream>>>(a, pp, qq, nodes, n, terms);
+    else if (vm == FM_O) k_inlet_terms<L, R, FM_E, FM_O><<<nb, 128, 0, a.stream>>>(a, pp, qq, nodes, n, terms);
+    else k_inlet_terms<L, R, FM_E, FM_E><<<nb, 128, 0, a.stream>>>(a, pp, qq, nodes, n, terms);
+  });
 }
 #endif
 #if defined(LBGPU_PART_TANGENT)
@@ -1748,15 +2141,24 @@ void tangent_terms(const Launch& a, int dim, int prec, const void* base, const v
 }
 #endif
 #if defined(LBGPU_PART_PRIMAL)
+// fm: the field's addressing mode (uploads into an in-place field land in O)
 void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in, void* out,
-            cudaStream_t st) {
+            cudaStream_t st, int fm) {
   const int bx = (g.x1 - g.x0) >= 128 ? 128 : 32;
   dim3 grid((g.x1 - g.x0 + bx - 1) / bx, g.ny, g.nz);
   LBGPU_LR_DISPATCH(dim, prec, {
-    if (field == 0 && to_ref) k_layout<L, R, -1, true><<<grid, bx, 0, st>>>(g, in, out);
-    else if (field == 0) k_layout<L, R, -1, false><<<grid, bx, 0, st>>>(g, in, out);
-    else if (to_ref) k_layout<L, R, +1, true><<<grid, bx, 0, st>>>(g, in, out);
-    else k_layout<L, R, +1, false><<<grid, bx, 0, st>>>(g, in, out);
+    if (!to_ref && fm != FM_DB) {
+      if (field == 0) k_layout<L, R, -1, false, FM_O><<<grid, bx, 0, st>>>(g, in, out);
+      else k_layout<L, R, +1, false, FM_O><<<grid, bx, 0, st>>>(g, in, out);
+    } else if (to_ref) {
+      LBGPU_FM_DISPATCH(fm, FM, {
+        if (field == 0) k_layout<L, R, -1, true, FM><<<grid, bx, 0, st>>>(g, in, out);
+        else k_layout<L, R, +1, true, FM><<<grid, bx, 0, st>>>(g, in, out);
+      });
+    } else {
+      if (field == 0) k_layout<L, R, -1, false><<<grid, bx, 0, st>>>(g, in, out);
+      else k_layout<L, R, +1, false><<<grid, bx, 0, st>>>(g, in, out);
+    }
   });
 }
 void halo(int op, const Geom& g, int dim, int prec, int field, void* buf, void* a, void* b,
@@ -1765,12 +2167,19 @@ void halo(int op, const Geom& g, int dim, int prec, int field, void* buf, void* 
   const unsigned nb = unsigned((yz + 127) / 128);
   LBGPU_LR_DISPATCH(dim, prec, {
     R* B = static_cast<R*>(buf);
-    if (op == 0) {  // pack into a (left), b (right)
-      if (field == 0) k_halo_pack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
+    // field 0: D = -1 (primal), 1: D = +1 (adjoint); ops 5 / 6 negate D (AA forward)
+    if (op == 0 || op == 5) {  // pack into a (left), b (right)
+      if ((field == 0) == (op == 0)) k_halo_pack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
       else k_halo_pack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
-    } else if (op == 1) {  // unpack from a (left), b (right)
-      if (field == 0) k_halo_unpack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
+    } else if (op == 1 || op == 6) {  // unpack from a (left), b (right)
+      if ((field == 0) == (op == 1)) k_halo_unpack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
       else k_halo_unpack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
+    } else if (op == 3) {  // AA reverse: pack the ghosts
+      if (field == 0) k_halo_rpack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
+      else k_halo_rpack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (R*)a, (R*)b);
+    } else if (op == 4) {  // AA reverse: unpack into the owned boundary columns
+      if (field == 0) k_halo_runpack<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
+      else k_halo_runpack<L, R, +1><<<nb, 128, 0, st>>>(g, B, (const R*)a, (const R*)b);
     } else {  // pull from neighbour buffers
       if (field == 0)
         k_halo_pull<L, R, -1><<<nb, 128, 0, st>>>(g, B, (const R*)left, gl, (const R*)right, gr);

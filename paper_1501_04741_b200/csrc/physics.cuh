@@ -65,6 +65,8 @@ struct Model {
   double beta_f, beta_s;
   double rho_in, rho_out;  // collision.hpp:57-58
   double u_clamp;
+  // fast build's pressure faces: 1/rho_in, 1/rho_out, 1/(1-u_clamp), 1/(1+u_clamp)
+  double inv_rho_in, inv_rho_out, inv_1m_uc, inv_1p_uc;
   double theta;
   int theta_int;      // theta when it is a small positive integer, else 0
   int fluid_power;    // SwitchingSpec::Form (topology.hpp:33-38)

@@ -62,6 +62,7 @@ struct SweepArgs {
   int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
   int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
   const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
+  int fm = 0, vm = 0;  // addressing modes of f and v: 0 double-buffered, 1/2 in place (O/E)
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).
@@ -72,15 +73,18 @@ struct SweepArgs {
   void adjoint_dual(const SweepArgs& s, const void* base, const void* src, void* dst);     \
   void gradient(const Launch& a, int dim, int prec, int ak, bool update, const void* p,    \
                 const void* q, const long long* nodes, long long n, double* gout,          \
-                double* w_rw, double zeta, double lambda, int accumulate);                 \
+                double* w_rw, double zeta, double lambda, int accumulate, int bm, int vm); \
   void objective_terms(const Launch& a, int dim, int prec, const void* p,                  \
-                       const long long* nodes, long long n, double* terms);                \
+                       const long long* nodes, long long n, double* terms, int bm);        \
   void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,       \
-                   const long long* nodes, long long n, double* terms);                    \
+                   const long long* nodes, long long n, double* terms, int bm, int vm);    \
   void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
-              void* out, cudaStream_t st);                                                 \
+              void* out, cudaStream_t st, int fm);                                         \
   void init_state(long long N, int dim, int prec, void* buf, cudaStream_t st);             \
-  void base_moments(const Launch& a, int dim, int prec, const void* base, void* mom);         \
+  void base_moments(const Launch& a, int dim, int prec, int bm, const void* base, void* mom); \
+  void primal_aa(const SweepArgs& s, void* A);                                             \
+  void adjoint_aa(const SweepArgs& s, const void* base, void* V);                          \
+  void pair_aa(const SweepArgs& s, void* F, void* V);                                      \
   void pair(const SweepArgs& s, const void* fsrc, void* fdst, const void* vsrc, void* vdst);  \
   void tangent(const SweepArgs& s, const void* base, const void* src, void* dst,              \
                const double* dw, double d_rho_in);                                           \

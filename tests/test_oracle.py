@@ -130,3 +130,37 @@ def test_reference_tangent_is_dual_to_adjoint(oracle_mod):
     dF, it, res, conv = r.tangent(dw, ddp, 1e-13, 400000)
     dot = float(g @ dw + gdp * ddp)
     assert conv and abs(dF - dot) <= 1e-10 * max(1.0, abs(dot))
+
+
+@pytest.mark.parametrize("name", ["mix3d", "grad2d"])
+def test_partitioned_runner_equals_monolithic(oracle_mod, name):
+    """ref_partitioned (the full-size parity oracle of test_gpu_fullsize.py)
+    is the reference's PartitionedRun: bitwise its monolithic operators
+    (test_partition.cpp:53-141), for primal, adjoint and pair sequences; and
+    objective_enabled(False) is the A14 recipe's obj_empty."""
+    O = oracle_mod
+    _need_ref(O)
+    txt = case_text(name)
+    a, b = O.RefOracle(txt), O.RefOracle(txt)
+    a.init_state()
+    b.init_state()
+    a.primal_steps(40)
+    b.primal_steps(40)
+    ra = a.partitioned(3, n_primal=9, n_adjoint=6, n_pairs=4)
+    b.set_state(1, np.zeros(b.m * b.n))
+    b.primal_steps(9)
+    b.adjoint_steps(6)
+    for _ in range(4):
+        rp = b.primal_steps(1)
+        rb = b.adjoint_steps(1)
+    assert ra == (rp, rb)
+    assert np.array_equal(a.get_state(0), b.get_state(0))
+    assert np.array_equal(a.get_state(1), b.get_state(1))
+    # obj_empty: an adjoint step from v = 0 without the source stays zero
+    a.set_state(1, np.zeros(a.m * a.n))
+    a.objective_enabled(False)
+    a.adjoint_steps(2)
+    assert not np.any(a.get_state(1))
+    a.objective_enabled(True)
+    a.adjoint_steps(1)
+    assert np.any(a.get_state(1))

@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Development probes on the GPU box (not the bench contract; bench.py is).
+
+  python tools/probe.py rates [C3 overrides key=value ...]
+      sweep / pair rates of one C3 variant (CUDA events)
+  python tools/probe.py geom
+      fused-pair rate with and without pressure faces (tags.geometry=periodic)
+  python tools/probe.py variants DIR
+      `rates` for every variant library DIR/*.so (built by
+      `LBGPU_NVCC_EXTRA=-D... LBGPU_BUILD_DIR=... LBGPU_LIB=DIR/x.so builder.py`),
+      one subprocess per library
+  python tools/probe.py ncu {pair,sweeps,gradient,aa}
+      a short run to put under ncu
+"""
+from __future__ import annotations
+
+import glob
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def _engine(ov: dict | None = None, cfg: str = "C3"):
+    import paper_1501_04741_b200 as P
+    from paper_1501_04741_b200.presets import config_text
+    e = P.Engine.from_config(config_text(cfg, ov or {}))
+    e.init_state()
+    e.primal_step(20, residual=False)
+    return e
+
+
+def rates(ov: dict, K: int = 100) -> dict:
+    e = _engine(ov)
+    s = 8 if e.precision == 64 else 4
+    m, n = e.m, e.n
+    e.time_pairs(5)
+    _, tp, ta = e.time_pairs(K)
+    e.time_pair_steps(5)
+    tpair = e.time_pair_steps(K)
+    e.time_sweeps(1, 5)
+    tf = e.time_sweeps(1, K)
+    out = {"lib": os.path.basename(os.environ.get("LBGPU_LIB", "liblbgpu.so")), "ov": ov,
+           "primal_gbs": round(2 * m * s * n * K / tp / 1e6, 1),
+           "adjoint_gbs": round(3 * m * s * n * K / ta / 1e6, 1),
+           "pair_mlups": round(n * K / tpair / 1e3, 1),
+           "pair_gbs": round((4 if s == 8 else 5) * m * s * n * K / tpair / 1e6, 1),
+           "frozen_adjoint_mlups": round(n * K / tf / 1e3, 1)}
+    e.close()
+    return out
+
+
+def kv(args):
+    ov = {}
+    for a in args:
+        k, v = a.split("=", 1)
+        ov[k] = v
+    return ov
+
+
+def main():
+    cmd = sys.argv[1] if len(sys.argv) > 1 else "rates"
+    if cmd == "rates":
+        print(json.dumps(rates(kv(sys.argv[2:]))), flush=True)
+    elif cmd == "geom":
+        for ov in ({}, {"tags.geometry": "periodic"}):
+            print(json.dumps(rates(ov)), flush=True)
+    elif cmd == "variants":
+        for lib in sorted(glob.glob(os.path.join(sys.argv[2], "*.so"))):
+            env = dict(os.environ, LBGPU_LIB=os.path.abspath(lib))
+            subprocess.run([sys.executable, __file__, "rates", *sys.argv[3:]], env=env, check=False)
+    elif cmd == "ncu":
+        what = sys.argv[2]
+        if what == "pair":
+            e = _engine()
+            e.pair_steps(4, residual=False)
+        elif what == "sweeps":
+            e = _engine()
+            e.adjoint_step(3, residual=False)
+        elif what == "gradient":
+            import numpy as np
+            e = _engine(cfg="C4")
+            e.one_shot(np.full(3, 1e-4), np.zeros(3), record_interval=100)
+        print("ok")
+
+
+if __name__ == "__main__":
+    main()
