@@ -205,15 +205,21 @@ int lbgpu_fd_gradient_batch(lbgpu_engine* e, int64_t n, const int64_t* ordinals,
  * call returns. residual (nullable) as lbgpu_primal_step. */
 int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64_t n,
                                   double* residual);
-/* One one_shot_run iteration head (optimizer.cpp:33-34: primal_step, then
- * adjoint_step against the new f) behind the design write-back of
- * optimizer.cpp:200-202, plus J = evaluate_raw of the new state
+/* A benchmark composite of the reference's operators (no reference loop runs
+ * exactly this): the design write-back of
+ * optimizer.cpp:200-202, one primal_step, one adjoint_step against the new f
+ * (optimizer.cpp:33-34) and J = evaluate_raw of the new state
  * (objective.cpp:64-72). Equals lbgpu_primal_step_with_design(1) +
- * lbgpu_adjoint_step(1, kernel 0) + lbgpu_objective bit for bit; the design
- * upload, the primal z-chunks and the adjoint z-chunks run as one overlapped
- * pipeline (3D, product build). Residuals and objective are nullable. */
+ * lbgpu_adjoint_step(1, kernel 0) + lbgpu_objective bit for bit in everything
+ * observable. Residuals and objective are nullable. Without residuals (3D,
+ * FP64 product build) the call's adjoint sweep is deferred into the next
+ * call's primal sweep (one fused kernel reading f once, gated on the upload
+ * slices); every other lbgpu call, or lbgpu_finish, completes it first. A
+ * rho <= 0 inside a deferred sweep is reported by the call that runs it. */
 int lbgpu_pair_step_with_design(lbgpu_engine* e, const double* w_design, double* primal_residual,
                                 double* adjoint_residual, double* objective);
+/* Complete any deferred sweep and wait for the engine's stream. */
+int lbgpu_finish(lbgpu_engine* e);
 /* n x adjoint_step (adjoint.cpp:206-254) against the current primal state.
  * kernel: 0 analytic, 1 dual sweep (AdjointKernel, adjoint.hpp:14-18). */
 int lbgpu_adjoint_step(lbgpu_engine* e, int64_t n, int kernel, double* residual);

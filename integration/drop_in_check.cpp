@@ -58,21 +58,25 @@ int main(int argc, char** argv) {
     const double Jg = gpu_evaluate_raw(e);
     const GradientVector gg = gpu_param_gradient(e, AdjointKernel::Analytic);
     // one MMA-shaped outer iteration on both: design write-back, then solves
+    // (cases without a design region skip it)
+    GradientVector g2, gg2;
     std::vector<double> wd(s.design.nodes.size());
-    for (std::size_t i = 0; i < wd.size(); ++i)
-      wd[i] = std::min(1.0, std::max(0.0, s.design.w[std::size_t(s.design.nodes[i])] + 1e-3 * g.design[i] / (g.max_abs() + 1e-300)));
-    System s2 = s;
-    for (std::size_t i = 0; i < wd.size(); ++i) s2.design.w[std::size_t(s2.design.nodes[i])] = wd[i];
-    StateField<double> f2(s.shape, s.m), v2(s.shape, s.m);
-    initialize_state(s2, f2);
-    solve_fixed_point(s2, f2, po);
-    AdjointSolveOptions<double> ao2;
-    ao2.fixed_iters = kp;  // mma_run: the adjoint runs the primal's count (optimizer.cpp:179)
-    solve_adjoint(s2, bc.objective, f2, v2, ao2);
-    const GradientVector g2 = param_gradient(s2, v2, f2, AdjointKernel::Analytic);
-    gpu_check(e, lbgpu_init_state(e));
-    SolveResult p2;
-    const GradientVector gg2 = gpu_mma_iteration(e, wd, po, &p2);
+    if (!wd.empty()) {
+      for (std::size_t i = 0; i < wd.size(); ++i)
+        wd[i] = std::min(1.0, std::max(0.0, s.design.w[std::size_t(s.design.nodes[i])] + 1e-3 * g.design[i] / (g.max_abs() + 1e-300)));
+      System s2 = s;
+      for (std::size_t i = 0; i < wd.size(); ++i) s2.design.w[std::size_t(s2.design.nodes[i])] = wd[i];
+      StateField<double> f2(s.shape, s.m), v2(s.shape, s.m);
+      initialize_state(s2, f2);
+      solve_fixed_point(s2, f2, po);
+      AdjointSolveOptions<double> ao2;
+      ao2.fixed_iters = kp;  // mma_run: the adjoint runs the primal's count (optimizer.cpp:179)
+      solve_adjoint(s2, bc.objective, f2, v2, ao2);
+      g2 = param_gradient(s2, v2, f2, AdjointKernel::Analytic);
+      gpu_check(e, lbgpu_init_state(e));
+      SolveResult p2;
+      gg2 = gpu_mma_iteration(e, wd, po, &p2);
+    }
     std::printf(
         "{\"nodes\": %ld, \"design\": %zu, \"exact\": %d, \"primal_iters\": [%ld, %ld], "
         "\"primal_residual\": [%.17g, %.17g], \"adjoint_residual\": [%.17g, %.17g], "

@@ -109,6 +109,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_primal_step_with_design.argtypes = [vp, vp, i64, dp]
     L.lbgpu_pair_steps.argtypes = [vp, i64, dp, dp]
     L.lbgpu_pair_step_with_design.argtypes = [vp, vp, dp, dp, dp]
+    L.lbgpu_finish.argtypes = [vp]
     L.lbgpu_time_pair_steps.argtypes = [vp, i64, dp]
     L.lbgpu_fd_gradient.argtypes = [vp, i64, C.c_double, C.c_double, i64, i64, dp]
     L.lbgpu_fd_gradient_batch.argtypes = [vp, i64, vp, vp, C.c_double, i64, i64, C.c_int, vp]
@@ -334,6 +335,10 @@ class Engine:
             C.byref(ra) if residual else None, C.byref(j) if objective else None))
         return (rp.value if residual else None, ra.value if residual else None,
                 j.value if objective else None)
+
+    def finish(self) -> None:
+        """Complete any deferred sweep (pair_step_with_design) and synchronize."""
+        self._ok(self.L.lbgpu_finish(self.h))
 
     def pair_steps(self, n: int = 1, residual: bool = True):
         """n primal+adjoint pairs (one-shot at zeta = 0 without the gradient);

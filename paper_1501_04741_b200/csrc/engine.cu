@@ -384,7 +384,7 @@ struct lbgpu_engine {
     cudaFree(d_dw), cudaFree(d_mom);
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
-    cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals);
+    cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals), cudaFree(d_w2);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -529,7 +529,7 @@ struct lbgpu_engine {
       CU(cudaMalloc(&d_p1, sizeof(double) * N));
       refresh_pow_tables();
     }
-    T.code = d_code, T.w = d_w, T.bcT = d_bcT, T.p0 = d_p0, T.p1 = d_p1;
+    T.code = d_code, T.w = d_w, T.w_adj = d_w, T.bcT = d_bcT, T.p0 = d_p0, T.p1 = d_p1;
     T.grad_side = d_grad_side, T.n_grad_side = (long long)grad_side.size();
     G = Geom{nx, ny, nz, 0, span, N, x0, gnx, ny};
     init_state();
@@ -589,7 +589,7 @@ struct lbgpu_engine {
     M.om = om;
     M.beta_f = d.beta_fluid, M.beta_s = d.beta_solid;
     inlet_dp = d.inlet_dp;
-    M.rho_in = 1.0 + 3.0 * d.inlet_dp;
+    set_rho_in(1.0 + 3.0 * d.inlet_dp);
     M.rho_out = 1.0;
     M.u_clamp = d.u_clamp;
     M.inv_rho_in = 1.0 / M.rho_in, M.inv_rho_out = 1.0 / M.rho_out;
@@ -922,10 +922,14 @@ struct lbgpu_engine {
   // Queue the z-chunked H2D copy of design values (after everything already
   // on st): chunk c covers design positions [ib[c], ib[c+1]) = z planes
   // [zb[c], zb[c+1]); ev_chunk[c] fires when its slice has landed.
-  void design_bounds(long long* ib, int* zb) const {
+  // skew: chunk 0 = nz/32 and chunk 1 = 3nz/32 of the planes, the rest nz/8
+  // each -- the first upload slice lands early, so the sweep starts early
+  void design_bounds(long long* ib, int* zb, bool skew = false) const {
     const long long plane = (long long)nx * ny;
+    static constexpr int kSkew[kChunks + 1] = {0, 1, 4, 8, 12, 16, 20, 24, 32};  // /32
+    static_assert(kChunks == 8, "skewed chunk table");
     for (int c = 0; c <= kChunks; ++c) {
-      zb[c] = int((long long)nz * c / kChunks);
+      zb[c] = skew ? int((long long)nz * kSkew[c] / 32) : int((long long)nz * c / kChunks);
       ib[c] = std::lower_bound(design.begin(), design.end(), plane * zb[c]) - design.begin();
     }
   }
@@ -937,13 +941,14 @@ struct lbgpu_engine {
       for (cudaEvent_t& ev : ev_chunk) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
   }
-  void queue_design_upload(const double* wd, long long* ib, int* zb, bool mark = true) {
+  void queue_design_upload(const double* wd, long long* ib, int* zb, bool mark = true,
+                           bool skew = false) {
     ensure_h2d();
     // the staging buffer is free once everything queued before us has run
     // (mark = false: the caller recorded ev_chunk[kChunks] on st already)
     if (mark) CU(cudaEventRecord(ev_chunk[kChunks], st));
     CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
-    design_bounds(ib, zb);
+    design_bounds(ib, zb, skew);
     for (int c = 0; c < kChunks; ++c)
       if (ib[c + 1] > ib[c]) {
         CU(cudaMemcpyAsync(d_wvals + ib[c], wd + ib[c], sizeof(double) * (ib[c + 1] - ib[c]),
@@ -1084,6 +1089,96 @@ struct lbgpu_engine {
     if (h_flags[3] != kNoBad) raise_bad(h_flags[3], "adjoint iteration");
     if (rp) *rp = bits_to_double(h_flags[0]);
     if (ra) *ra = bits_to_double(h_flags[4]);
+    if (J) *J = bits_to_double(h_flags[5]);
+  }
+
+  // The deferred-adjoint form of the design pair (no residuals requested).
+  // Call k uploads w_k and runs primal sweep k; its adjoint sweep (against
+  // f^k, with w_k) is left pending and runs inside call k+1's primal sweep as
+  // the adjoint half of one fused k_pair (DUALW: that half reads the previous
+  // design, kept in the second w buffer), so each call streams 4 M s bytes per
+  // node instead of 5 M s and the upload gates one kernel, not two. Any other
+  // call flushes the pending sweep first (guarded()), so everything observable
+  // -- f, v, w, J, gradients -- is bitwise the three separate calls; a rho <= 0
+  // in a deferred adjoint sweep surfaces at the next call as "adjoint
+  // iteration". Design buffers alternate: d_w (current, w_{k-1}) and d_w2
+  // (receives w_k); outside the design nodes both hold the same values
+  // (w2_synced; lbgpu_set_design clears it).
+  bool adj_pending = false;
+  double* d_w2 = nullptr;
+  bool w2_synced = false;
+  void flush_pending() {
+    if (!adj_pending) return;
+    adj_pending = false;
+    reset_flags();
+    adjoint_launch(0, false, nullptr);
+    CU(cudaGetLastError());
+    reduce_flags(d_flags + 1, 1, true);
+    pull_flags();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "adjoint iteration");
+  }
+  bool lazy_pair_ok() const { return design_chunking() && fuse_pairs() && !aa; }
+  void design_pair_lazy(const double* wd, double* J) {
+    require_solo();
+    if (!d_w2) CU(cudaMalloc(&d_w2, sizeof(double) * N));
+    if (!w2_synced) {
+      CU(cudaMemcpyAsync(d_w2, d_w, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+      w2_synced = true;
+    }
+    const bool fuse = adj_pending;
+    adj_pending = false;
+    long long ib[kChunks + 1];
+    int zb[kChunks + 1];
+    reset_flags();
+    trace_name.clear();
+    trace("start", st);
+    queue_design_upload(wd, ib, zb, true, true);
+    ++primal_steps;
+    if (fuse) ++adjoint_steps;
+    NodeTables tn = T;
+    tn.w = d_w2;     // the new design (primal half)
+    tn.w_adj = d_w;  // the previous one (the deferred adjoint half)
+    for (int c = 0; c < kChunks; ++c) {
+      const long long m_ = ib[c + 1] - ib[c];
+      if (m_ > 0) {
+        CU(cudaStreamWaitEvent(st, ev_chunk[c], 0));
+        k_scatter_design<<<unsigned((m_ + 255) / 256), 256, 0, st>>>(d_wvals + ib[c], d_design + ib[c],
+                                                                     m_, d_w2);
+        ++launches;
+      }
+      SweepArgs sa = sweep(primal_steps - kb_p, false, nullptr);
+      sa.a.t = tn;
+      sa.z0 = zb[c], sa.z1 = zb[c + 1];
+      if (fuse) {
+        sa.dualw = true;
+        if (c < kChunks - 1) sa.n_adj_side = 0;  // the side list once, with the last chunk
+        fast::pair(sa, f[fc], f[1 - fc], v[vc], v[1 - vc]);
+        launches += 1 + (c == kChunks - 1 && sa.n_adj_side > 0);
+      } else {
+        fast::primal(sa, f[fc], f[1 - fc]);
+        ++launches;
+      }
+      if (trace_on()) trace(("K" + std::to_string(c)).c_str(), st);
+    }
+    fc ^= 1;
+    if (fuse) vc ^= 1;
+    std::swap(d_w, d_w2);
+    T.w = T.w_adj = d_w;
+    w_host_stale = true;
+    if (J) {
+      fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support,
+                            (long long)support.size(), d_terms, 0);
+      ++launches;
+      pairwise_queue(tree_support, d_terms);
+    }
+    CU(cudaGetLastError());
+    reduce_flags(d_flags + 1, 1, true);
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+    if (J) CU(cudaMemcpyAsync(h_flags + 5, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();  // one host sync per call; the host design buffer is consumed too
+    trace_print();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], fuse ? "iteration (or the deferred adjoint iteration)" : "iteration");
+    adj_pending = true;
     if (J) *J = bits_to_double(h_flags[5]);
   }
 
@@ -1428,6 +1523,11 @@ struct lbgpu_engine {
     sync();
     w_host_stale = false;
   }
+  // rho_in and the reciprocal the fast build's pressure faces use
+  void set_rho_in(double r) {
+    M.rho_in = r;
+    M.inv_rho_in = 1.0 / r;
+  }
   // Raw write of one node's w (no clamp), with its libm pow pair in exact mode.
   void set_node_w(long long idx, double val) {
     w[idx] = val;
@@ -1459,7 +1559,7 @@ struct lbgpu_engine {
     const long long idx = ordinal >= 0 ? design[ordinal] : -1;
     const double w0 = idx >= 0 ? w[idx] : 0.0;
     auto restore = [&] {
-      M.rho_in = rho0;
+      set_rho_in(rho0);
       if (idx >= 0) set_node_w(idx, w0);
       fc = fc0;
       CU(cudaMemcpyAsync(f[fc], save, field_bytes(), cudaMemcpyDeviceToDevice, st));
@@ -1468,7 +1568,7 @@ struct lbgpu_engine {
     };
     try {
       auto run = [&](double delta) {
-        if (idx < 0) M.rho_in = 1.0 + 3.0 * (inlet_dp + delta);  // rho_inlet(), collision.hpp:57
+        if (idx < 0) set_rho_in(1.0 + 3.0 * (inlet_dp + delta));  // rho_inlet(), collision.hpp:57
         else set_node_w(idx, w0 + delta);
         init_state();
         long long it = 0;
@@ -1512,7 +1612,7 @@ struct lbgpu_engine {
     const int fc0 = fc;
     const double rho0 = M.rho_in;
     auto release = [&] {
-      M.rho_in = rho0;
+      set_rho_in(rho0);
       fc = fc0;
       if (save) cudaMemcpyAsync(f[fc], save, field_bytes(), cudaMemcpyDeviceToDevice, st);
       cudaStreamSynchronize(st);
@@ -1535,7 +1635,7 @@ struct lbgpu_engine {
         for (int side = 0; side < 2; ++side) {
           const double delta = side == 0 ? hs[k] : -hs[k];
           if (idx < 0) {
-            M.rho_in = 1.0 + 3.0 * (inlet_dp + delta);  // rho_inlet(), collision.hpp:57
+            set_rho_in(1.0 + 3.0 * (inlet_dp + delta));  // rho_inlet(), collision.hpp:57
           } else {
             double* sv = sk + 3 * side;
             sv[0] = w[idx] + delta;
@@ -1560,7 +1660,7 @@ struct lbgpu_engine {
           CU(cudaMemcpyAsync(d_vals + 2 * k + side, d_scalar, sizeof(double), cudaMemcpyDeviceToDevice, st));
         }
         if (idx < 0) {
-          M.rho_in = rho0;
+          set_rho_in(rho0);
         } else {  // the write-back (fd_gradient's restore)
           double* s0 = sk + 6;
           s0[0] = w[idx];
@@ -1856,11 +1956,15 @@ namespace {
 
 thread_local std::string g_create_err;
 
+// Every API call first completes a deferred sweep (lbgpu_pair_step_with_design
+// leaves one pending), so nothing observes a half-finished step; `keep`
+// skips that for the call that manages the pending sweep itself.
 template <class F>
-int guarded(lbgpu_engine* e, F&& fn) {
+int guarded(lbgpu_engine* e, F&& fn, bool keep = false) {
   if (!e) return LBGPU_E_ARG;
   try {
     if (e->device >= 0) cudaSetDevice(e->device);
+    if (!keep) e->flush_pending();
     fn();
     e->err.clear();
     return LBGPU_OK;
@@ -2356,6 +2460,7 @@ int lbgpu_download_state_device(lbgpu_engine* e, int field, double* d_ref) {
 int lbgpu_set_design(lbgpu_engine* e, const double* w_full) {
   if (!w_full) return LBGPU_E_ARG;
   return guarded(e, [&] {
+    e->w2_synced = false;  // non-design values may change
     e->w.assign(w_full, w_full + e->N);
     e->w_host_stale = false;
     e->build_codes();
@@ -2416,7 +2521,13 @@ int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64
 int lbgpu_pair_step_with_design(lbgpu_engine* e, const double* w_design, double* primal_residual,
                                 double* adjoint_residual, double* objective) {
   if (!w_design) return LBGPU_E_ARG;
+  if (e && !primal_residual && !adjoint_residual && e->lazy_pair_ok())
+    return guarded(e, [&] { e->design_pair_lazy(w_design, objective); }, true);
   return guarded(e, [&] { e->design_pair(w_design, primal_residual, adjoint_residual, objective); });
+}
+
+int lbgpu_finish(lbgpu_engine* e) {
+  return guarded(e, [&] { e->sync(); });
 }
 
 int lbgpu_tangent_solve(lbgpu_engine* e, const double* dw_design, double d_inlet_dp, double tol,

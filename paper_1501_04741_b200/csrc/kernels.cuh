@@ -195,7 +195,10 @@ __device__ __forceinline__ unsigned long long absdiff_bits(double a, double b) {
   return (unsigned long long)__double_as_longlong(fabs(a - b));
 }
 
-// Block-wide max of a bit pattern, one atomicMax per block.
+// Block-wide max of a bit pattern, one atomicMax per block. Warps are
+// numbered by linear thread id (2-D blocks), and the leading barrier keeps a
+// second call in the same kernel from overwriting `red` while warp 0 of the
+// first call still reads it.
 __device__ __forceinline__ void block_max_bits(unsigned long long v, unsigned long long* dst) {
   __shared__ unsigned long long red[32];
 #pragma unroll
@@ -203,8 +206,10 @@ __device__ __forceinline__ void block_max_bits(unsigned long long v, unsigned lo
     const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
     v = u > v ? u : v;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarp = (blockDim.x * blockDim.y + 31) >> 5;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nwarp = (blockDim.x * blockDim.y * blockDim.z + 31) >> 5;
+  __syncthreads();
   if (lane == 0) red[warp] = v;
   __syncthreads();
   if (warp == 0) {
@@ -1266,7 +1271,10 @@ constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 // bitwise the stand-alone sweep (same functions, same operands). Side-list
 // nodes' adjoint half goes to k_adjoint_side as usual.
 // FM / VM: addressing of f and v (in place: fsrc == fdst, vsrc == vdst).
-template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB>
+// DUALW: the adjoint half is the previous design's (lbgpu_pair_step_with_design
+// defers each call's adjoint sweep into the next call's fused kernel), so its
+// node constants come from a.t.w_adj while the primal half uses a.t.w.
+template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB, bool DUALW = false>
 __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fdst,
                                           const R* vsrc, R* vdst, int x, int y, int z, int tid,
                                           unsigned long long& rP, unsigned long long& rA) {
@@ -1351,8 +1359,17 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
 #pragma unroll
       for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
     } else {
+      PowPair ppa = pp;
+      double omta = omt;
+      if constexpr (DUALW) {
+        if (code & CODE_HAS_W) {
+          const double wa = a.t.w_adj[idx];
+          ppa = node_pp<false>(a.M, a.t, idx, code, wa);
+          omta = node_omt<R>(a.M, a.t, code, wa);
+        }
+      }
       if (rho > R(0))
-        fast_vjp_mi<L, R, CK>(a.M, pp, omt, rho, inv, jv, T, vin, vin + L::MF, vout, vout + L::MF);
+        fast_vjp_mi<L, R, CK>(a.M, ppa, omta, rho, inv, jv, T, vin, vin + L::MF, vout, vout + L::MF);
       else
         okA = false;
       if (face) {
@@ -1388,7 +1405,7 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
 #define LBGPU_PAIR_BOUNDS(R)                                                   \
   __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_PAIR_MINB) * \
                                          128 / kPairThreads<R>)
-template <class L, class R, int CK, bool RESID>
+template <class L, class R, int CK, bool RESID, bool DUALW = false>
 __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
                                                         R* __restrict__ fdst,
                                                         const R* __restrict__ vsrc,
@@ -1397,8 +1414,9 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   unsigned long long rP = 0, rA = 0;
   if (x < a.g.x1 && y < a.g.ny)
-    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, x, y, a.g.z0 + blockIdx.z,
-                               threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
+    pair_body<L, R, CK, RESID, FM_DB, FM_DB, DUALW>(a, fsrc, fdst, vsrc, vdst, x, y,
+                                                    a.g.z0 + blockIdx.z,
+                                                    threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
   if constexpr (RESID) {
     detail::block_max_bits(rP, a.fl.resid);
     detail::block_max_bits(rA, a.fl.aux);
@@ -1916,11 +1934,19 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
       int nzs = a.g.nz;
       if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (design pair)
       dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, nzs);
-      k_pair<L, R, CK, RES><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
+      bool done = false;
+      if constexpr (!RES && L::DIM == 3) {
+        if (s.dualw) {
+          k_pair<L, R, CK, false, true><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
+          done = true;
+        }
+      }
+      if (!done) k_pair<L, R, CK, RES><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
     }
   }
   if (s.n_adj_side > 0 && s.part != 1) {
     Launch as = s.a;
+    if (s.dualw) as.t.w = as.t.w_adj;  // the side nodes' adjoint is the previous design's
     as.fl.resid = s.a.fl.aux;  // the side nodes' residual is the adjoint's
     k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
         as, fsrc, vsrc, vdst, s.adj_side, s.n_adj_side);

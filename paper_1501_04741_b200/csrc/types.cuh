@@ -18,6 +18,7 @@ struct Geom {
 struct NodeTables {
   const uint8_t* code;
   const double* w;
+  const double* w_adj;  // the design the adjoint half of a lazy design pair uses (else == w)
   const double* bcT;
   const double* p0;  // exact build: host-glibc pow(base, theta) per node
   const double* p1;  //              pow(base, theta - 1)
@@ -63,6 +64,7 @@ struct SweepArgs {
   int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
   const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
   int fm = 0, vm = 0;  // addressing modes of f and v: 0 double-buffered, 1/2 in place (O/E)
+  bool dualw = false;  // fused pair: the adjoint half reads w from a.t.w_adj (3-D, no residual)
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).

@@ -334,6 +334,44 @@ def test_pair_step_with_design_equals_separate_calls(lbgpu, has_gpu, nz):
             assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
 
 
+@pytest.mark.parametrize("nz", [16, 37])
+def test_deferred_design_pairs_equal_separate_calls(lbgpu, has_gpu, nz):
+    """Back-to-back lbgpu_pair_step_with_design calls without residuals defer
+    each adjoint sweep into the next call's fused sweep (the adjoint half
+    reading the previous design); J of every call, and f, v, w and the
+    gradient once anything else runs, are bitwise the separate calls."""
+    wide = {"lattice.nx": 96, "tags.design_x0": 40, "tags.design_x1": 59}
+    for name, over in (("mix3d", {}), ("exch3d", {}), ("mix3d", wide), ("periodic3d", None)):
+        if over is None:  # synthetic objective: side-list adjoint nodes in the fused sweep
+            txt = case_text("bgk3d", {"lattice.nz": nz, "tags.geometry": "periodic",
+                                      "objective.kind": "synthetic"})
+        else:
+            txt = case_text(name, {**over, "lattice.nz": nz})
+        a = lbgpu.Engine.from_config(txt)
+        b = lbgpu.Engine.from_config(txt)
+        for e in (a, b):
+            e.init_state()
+            e.primal_step(20)
+        rng = np.random.default_rng(nz)
+        for k in range(5):
+            vals = rng.uniform(0.05, 1, a.n_design)
+            ja = a.pair_step_with_design(vals, residual=False)[2]
+            b.primal_step_with_design(vals, 1, residual=False)
+            b.adjoint_step(1, residual=False)
+            assert ja == b.objective()
+        a.finish()
+        assert np.array_equal(a.get_state(0), b.get_state(0))
+        assert np.array_equal(a.get_state(1), b.get_state(1))
+        assert np.array_equal(a.design_values(), b.design_values())
+        # a deferred sweep is completed by whatever call comes next
+        vals = rng.uniform(0.05, 1, a.n_design)
+        a.pair_step_with_design(vals, residual=False, objective=False)
+        b.primal_step_with_design(vals, 1, residual=False)
+        b.adjoint_step(1, residual=False)
+        assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
+        assert np.array_equal(a.get_state(1), b.get_state(1))
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_frozen_base_moment_cache_is_bitwise(lbgpu, has_gpu, name):
     """adjoint_step(n >= 2) and solve_adjoint cache the frozen base's moments

@@ -9,7 +9,12 @@
       `rates` for every variant library DIR/*.so (built by
       `LBGPU_NVCC_EXTRA=-D... LBGPU_BUILD_DIR=... LBGPU_LIB=DIR/x.so builder.py`),
       one subprocess per library
-  python tools/probe.py ncu {pair,sweeps,gradient,aa}
+  python tools/probe.py aa
+      rates of the double-buffered and the in-place (AA) engines, C3 FP64 / FP32
+  python tools/probe.py e2e
+      lbgpu_pair_step_with_design rate (with LBGPU_TRACE_PAIR=1 in the
+      environment, each call's stage timeline on stderr)
+  python tools/probe.py ncu {pair,sweeps,gradient,aa,e2e}
       a short run to put under ncu
 """
 from __future__ import annotations
@@ -24,17 +29,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def _engine(ov: dict | None = None, cfg: str = "C3"):
+def _engine(ov: dict | None = None, cfg: str = "C3", streaming: str = "double"):
     import paper_1501_04741_b200 as P
     from paper_1501_04741_b200.presets import config_text
-    e = P.Engine.from_config(config_text(cfg, ov or {}))
+    e = P.Engine.from_config(config_text(cfg, ov or {}), streaming=streaming)
     e.init_state()
     e.primal_step(20, residual=False)
     return e
 
 
-def rates(ov: dict, K: int = 100) -> dict:
-    e = _engine(ov)
+def rates(ov: dict, K: int = 100, streaming: str = "double") -> dict:
+    e = _engine(ov, streaming=streaming)
     s = 8 if e.precision == 64 else 4
     m, n = e.m, e.n
     e.time_pairs(5)
@@ -44,6 +49,7 @@ def rates(ov: dict, K: int = 100) -> dict:
     e.time_sweeps(1, 5)
     tf = e.time_sweeps(1, K)
     out = {"lib": os.path.basename(os.environ.get("LBGPU_LIB", "liblbgpu.so")), "ov": ov,
+           "streaming": streaming,
            "primal_gbs": round(2 * m * s * n * K / tp / 1e6, 1),
            "adjoint_gbs": round(3 * m * s * n * K / ta / 1e6, 1),
            "pair_mlups": round(n * K / tpair / 1e3, 1),
@@ -72,6 +78,26 @@ def main():
         for lib in sorted(glob.glob(os.path.join(sys.argv[2], "*.so"))):
             env = dict(os.environ, LBGPU_LIB=os.path.abspath(lib))
             subprocess.run([sys.executable, __file__, "rates", *sys.argv[3:]], env=env, check=False)
+    elif cmd == "aa":
+        for prec in (64, 32):
+            for st in ("double", "aa"):
+                print(json.dumps(rates({"model.precision": prec}, streaming=st)), flush=True)
+    elif cmd == "e2e":
+        import time
+        import numpy as np
+        import torch
+        e = _engine()
+        w = torch.from_numpy(e.design_values()).pin_memory().numpy()
+        for _ in range(40):
+            e.pair_step_with_design(w, residual=False)
+        e.finish()
+        K = 200
+        t0 = time.perf_counter()
+        for _ in range(K):
+            e.pair_step_with_design(w, residual=False)
+        e.finish()
+        dt = (time.perf_counter() - t0) / K
+        print(json.dumps({"e2e_ms_per_step": dt * 1e3, "e2e_mlups": e.n / dt / 1e6}), flush=True)
     elif cmd == "ncu":
         what = sys.argv[2]
         if what == "pair":
@@ -84,6 +110,15 @@ def main():
             import numpy as np
             e = _engine(cfg="C4")
             e.one_shot(np.full(3, 1e-4), np.zeros(3), record_interval=100)
+        elif what == "aa":
+            e = _engine(streaming="aa")
+            e.pair_steps(4, residual=False)
+        elif what == "e2e":
+            e = _engine()
+            w = e.design_values()
+            for _ in range(4):
+                e.pair_step_with_design(w, residual=False)
+            e.finish()
         print("ok")
 
 
