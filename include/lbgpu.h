@@ -276,9 +276,15 @@ int lbgpu_group_link(lbgpu_engine** engines, int n);
  * waits only on its two neighbours' previous sweep. Same lbgpu_group_* calls. */
 int lbgpu_group_link_p2p(lbgpu_engine** engines, int n);
 /* which: 0 primal, 1 adjoint (kernel as lbgpu_adjoint_step); residual =
- * global max-norm step residual of the last step (nullable). */
+ * global max-norm step residual of the last step (nullable). P2P groups also
+ * take which = 2: fused primal+adjoint pairs (as lbgpu_pair_steps: adjoint
+ * k with primal k+1 in one sweep, both fields' cut planes pushed; residual
+ * NULL). */
 int lbgpu_group_step(lbgpu_engine** engines, int n, int which, int64_t steps, int kernel,
                      double* residual);
+/* P2P group: milliseconds of `steps` lock steps (which as lbgpu_group_step),
+ * CUDA events on every slab's stream, the maximum over slabs. */
+int lbgpu_group_time(lbgpu_engine** engines, int n, int which, int64_t steps, double* ms);
 /* Fill every slab's ghost columns of `field` (after uploads). */
 int lbgpu_group_exchange(lbgpu_engine** engines, int n, int field);
 /* NCCL (one slab per rank, one GPU per rank): rank 0 makes the id, every rank

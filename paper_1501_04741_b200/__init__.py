@@ -133,6 +133,7 @@ def load_library() -> C.CDLL:
     L.lbgpu_group_link.argtypes = [C.POINTER(vp), C.c_int]
     L.lbgpu_group_link_p2p.argtypes = [C.POINTER(vp), C.c_int]
     L.lbgpu_group_step.argtypes = [C.POINTER(vp), C.c_int, C.c_int, i64, C.c_int, dp]
+    L.lbgpu_group_time.argtypes = [C.POINTER(vp), C.c_int, C.c_int, i64, dp]
     L.lbgpu_group_exchange.argtypes = [C.POINTER(vp), C.c_int, C.c_int]
     L.lbgpu_nccl_unique_id.argtypes = [vp, C.c_int]
     L.lbgpu_attach_nccl.argtypes = [vp, vp, C.c_int, C.c_int]
@@ -530,10 +531,28 @@ class SlabGroup:
         for e in self.engines:
             e.init_state()
 
-    def step(self, which: int, steps: int = 1, kernel: int = 0) -> float:
+    def step(self, which: int, steps: int = 1, kernel: int = 0, residual: bool = True):
+        """which: 0 primal, 1 adjoint, 2 fused pair sweeps (P2P groups; no
+        residual). Returns the global residual of the last step, or None."""
         r = C.c_double()
-        self._ok(self.L.lbgpu_group_step(self._arr, self.n, which, steps, kernel, C.byref(r)))
-        return r.value
+        self._ok(self.L.lbgpu_group_step(self._arr, self.n, which, steps, kernel,
+                                         C.byref(r) if residual and which != 2 else None))
+        return r.value if residual and which != 2 else None
+
+    def pair_steps(self, n: int = 1) -> None:
+        """lbgpu_pair_steps over the group: primal, n-1 fused pair sweeps, adjoint."""
+        if n <= 0:
+            return
+        self.step(0, 1, residual=False)
+        if n > 1:
+            self.step(2, n - 1)
+        self.step(1, 1, residual=False)
+
+    def time(self, which: int, steps: int) -> float:
+        """P2P group: milliseconds of `steps` lock steps (max over slabs)."""
+        ms = C.c_double()
+        self._ok(self.L.lbgpu_group_time(self._arr, self.n, which, steps, C.byref(ms)))
+        return ms.value
 
     def exchange(self, field: int):
         self._ok(self.L.lbgpu_group_exchange(self._arr, self.n, field))

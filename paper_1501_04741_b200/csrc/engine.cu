@@ -299,8 +299,8 @@ struct lbgpu_engine {
                                     " needs the double-buffered state (in-place streaming keeps "
                                     "no previous state for the step residual)"};
   }
-  void* push_dst_l = nullptr;  // xmode 3: this sweep's neighbour destinations
-  void* push_dst_r = nullptr;
+  void* push_dst_l[2] = {nullptr, nullptr};  // xmode 3: this sweep's neighbour destinations
+  void* push_dst_r[2] = {nullptr, nullptr};  // ([0] primal field, [1] adjoint field)
   cudaEvent_t ev_step[2] = {nullptr, nullptr};  // xmode 3: sweep k done (parity k)
   long long gstep = 0;
   lbgpu_engine* nb_left = nullptr;
@@ -385,6 +385,8 @@ struct lbgpu_engine {
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
     cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals), cudaFree(d_w2);
+    cudaFree(d_gate_flags);
+    if (h_gate_seq) cudaFreeHost(h_gate_seq);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -797,8 +799,9 @@ struct lbgpu_engine {
   Push push_targets() const {
     Push p;
     if (xmode != 3) return p;
-    p.l_dst = push_dst_l, p.l_col = nb_left->span, p.l_nx = nb_left->nx, p.l_N = nb_left->N;
-    p.r_dst = push_dst_r, p.r_col = nb_right->nx - 1, p.r_nx = nb_right->nx, p.r_N = nb_right->N;
+    for (int k = 0; k < 2; ++k) p.l_dst[k] = push_dst_l[k], p.r_dst[k] = push_dst_r[k];
+    p.l_col = nb_left->span, p.l_nx = nb_left->nx, p.l_N = nb_left->N;
+    p.r_col = nb_right->nx - 1, p.r_nx = nb_right->nx, p.r_N = nb_right->N;
     return p;
   }
   void primal_launch(bool resid, unsigned long long* slot, bool exch = true) {
@@ -1107,6 +1110,69 @@ struct lbgpu_engine {
   bool adj_pending = false;
   double* d_w2 = nullptr;
   bool w2_synced = false;
+  // Upload-gated single launch (kernels.cuh Gate): when the design nodes are
+  // exactly a box (config-built cases: interior x the design x-range), the
+  // fused sweep of a deferred pair is ONE launch whose blocks wait on
+  // per-slice flags the copy engine sets behind each slice of the upload --
+  // no z-chunk kernel boundaries, no scatter kernels.
+  static constexpr int kSlices = 16;
+  int gate_state = -1;  // -1 unknown, 0 no box, 1 box
+  Gate gate_box{};
+  unsigned* d_gate_flags = nullptr;
+  unsigned* h_gate_seq = nullptr;  // pinned source of the flag values
+  unsigned gate_seq = 0;
+  bool gate_ready() {
+    if (gate_state >= 0) return gate_state == 1;
+    gate_state = 0;
+    if (design.empty() || ghosts) return false;
+    int x0_ = nx, x1_ = -1, y0_ = ny, y1_ = -1, z0_ = nz, z1_ = -1;
+    for (long long i : design) {
+      const int x = int(i % nx), y = int((i / nx) % ny), z = int(i / ((long long)nx * ny));
+      x0_ = std::min(x0_, x), x1_ = std::max(x1_, x), y0_ = std::min(y0_, y), y1_ = std::max(y1_, y);
+      z0_ = std::min(z0_, z), z1_ = std::max(z1_, z);
+    }
+    const long long vol = (long long)(x1_ - x0_ + 1) * (y1_ - y0_ + 1) * (z1_ - z0_ + 1);
+    if (vol != (long long)design.size()) return false;  // not a box: the chunked path
+    gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
+    gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
+    gate_box.slices = std::min(kSlices, z1_ - z0_ + 1);
+    CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * kSlices));
+    CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * kSlices));
+    CU(cudaMallocHost(&h_gate_seq, sizeof(unsigned) * kSlices));
+    gate_state = 1;
+    return true;
+  }
+  // The gated fused sweep of a deferred pair (adj_pending): upload slices +
+  // flags on the copy stream, one k_pair launch on st.
+  void gated_pair(const double* wd) {
+    ensure_h2d();
+    CU(cudaEventRecord(ev_chunk[kChunks], st));  // the previous call's readers of d_wvals are done
+    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
+    ++gate_seq;
+    const int ns = gate_box.slices, nzb = gate_box.bz1 - gate_box.bz0;
+    const long long plane = (long long)(gate_box.bx1 - gate_box.bx0) * (gate_box.by1 - gate_box.by0);
+    for (int c = 0; c < ns; ++c) {
+      const long long p0 = ((long long)c * nzb + ns - 1) / ns, p1 = ((long long)(c + 1) * nzb + ns - 1) / ns;
+      if (p1 > p0)
+        CU(cudaMemcpyAsync(d_wvals + p0 * plane, wd + p0 * plane, sizeof(double) * (p1 - p0) * plane,
+                           cudaMemcpyHostToDevice, st_h2d));
+      h_gate_seq[c] = gate_seq;
+      CU(cudaMemcpyAsync(d_gate_flags + c, h_gate_seq + c, sizeof(unsigned), cudaMemcpyHostToDevice,
+                         st_h2d));
+    }
+    NodeTables tn = T;
+    tn.w = d_w2;     // the new design's full-grid buffer (design nodes written by the sweep)
+    tn.w_adj = d_w;  // the previous design (the deferred adjoint half)
+    SweepArgs sa = sweep(primal_steps - kb_p, false, nullptr);
+    sa.a.t = tn;
+    sa.a.gate = gate_box;
+    sa.a.gate.wd = d_wvals, sa.a.gate.w_out = d_w2, sa.a.gate.flags = d_gate_flags;
+    sa.a.gate.seq = gate_seq;
+    sa.dualw = true;
+    fast::pair(sa, f[fc], f[1 - fc], v[vc], v[1 - vc]);
+    launches += 1 + (sa.n_adj_side > 0);
+    if (trace_on()) trace("K", st);
+  }
   void flush_pending() {
     if (!adj_pending) return;
     adj_pending = false;
@@ -1132,13 +1198,19 @@ struct lbgpu_engine {
     reset_flags();
     trace_name.clear();
     trace("start", st);
-    queue_design_upload(wd, ib, zb, true, true);
     ++primal_steps;
     if (fuse) ++adjoint_steps;
+    const bool gated = fuse && gate_ready();
+    if (gated) {
+      ensure_h2d();
+      gated_pair(wd);
+    } else {
+      queue_design_upload(wd, ib, zb, true, true);
+    }
     NodeTables tn = T;
     tn.w = d_w2;     // the new design (primal half)
     tn.w_adj = d_w;  // the previous one (the deferred adjoint half)
-    for (int c = 0; c < kChunks; ++c) {
+    for (int c = 0; c < (gated ? 0 : kChunks); ++c) {
       const long long m_ = ib[c + 1] - ib[c];
       if (m_ > 0) {
         CU(cudaStreamWaitEvent(st, ev_chunk[c], 0));
@@ -1287,6 +1359,7 @@ struct lbgpu_engine {
     void* vd = v[1 - vc];
     const void* fsrc = f[fc];
     const void* vsrc = v[vc];
+    s.a.push = push_targets();
     auto go = [&](const SweepArgs& a) { fast::pair(a, fsrc, fd, vsrc, vd); };
     if (xmode == 2) {
       SweepArgs b = s;
@@ -2085,53 +2158,63 @@ int lbgpu_group_exchange(lbgpu_engine** es, int n, int field) {
   return LBGPU_OK;
 }
 
+// One lock step of a P2P group (which: 0 primal, 1 adjoint, 2 fused pair:
+// adjoint k + primal k+1, both fields pushed): each slab's sweep waits on
+// its two neighbours' previous sweep (their ghosts are read-complete, WAR, and
+// the planes they pushed into mine are written, RAW), then records its own.
+static void p2p_sweep(lbgpu_engine** es, int n, int which, int kernel, bool r) {
+  const int fpar = es[0]->fc, vpar = es[0]->vc;  // lock step: same parities everywhere
+  for (int i = 0; i < n; ++i) {
+    lbgpu_engine* e = es[i];
+    CU(cudaSetDevice(e->device));
+    for (int k = 0; k < 2; ++k) e->push_dst_l[k] = e->push_dst_r[k] = nullptr;
+    if (which != 1) {  // the primal field's next buffer
+      e->push_dst_l[0] = e->nb_left->f[1 - fpar];
+      e->push_dst_r[0] = e->nb_right->f[1 - fpar];
+    }
+    if (which != 0) {  // the adjoint field's
+      e->push_dst_l[1] = e->nb_left->v[1 - vpar];
+      e->push_dst_r[1] = e->nb_right->v[1 - vpar];
+    }
+    const int prev = int((e->gstep + 1) & 1);
+    CU(cudaStreamWaitEvent(e->st, e->nb_left->ev_step[prev], 0));
+    CU(cudaStreamWaitEvent(e->st, e->nb_right->ev_step[prev], 0));
+    if (which == 0) e->primal_launch(r, nullptr, false);
+    else if (which == 1) e->adjoint_launch(kernel, r, nullptr, false);
+    else e->fused_pair_raw(r);
+    CU(cudaEventRecord(e->ev_step[e->gstep & 1], e->st));
+  }
+  for (int i = 0; i < n; ++i) ++es[i]->gstep;
+}
+
 int lbgpu_group_step(lbgpu_engine** es, int n, int which, int64_t steps, int kernel,
                      double* residual) {
-  if (!es || n < 1 || steps < 0 || (which != 0 && which != 1)) return LBGPU_E_ARG;
+  if (!es || n < 1 || steps < 0 || which < 0 || which > 2) return LBGPU_E_ARG;
   if (n > 1 && es[0] && es[0]->xmode == 3) {
     for (int i = 0; i < n; ++i)
       if (!es[i] || es[i]->xmode != 3) return LBGPU_E_STATE;
+    if (which == 2 && (residual || !es[0]->fuse_pairs())) return LBGPU_E_STATE;
     return guarded(es[0], [&] {
       for (int i = 0; i < n; ++i) {  // whatever each slab had queued (uploads, init) lands first
         CU(cudaSetDevice(es[i]->device));
         es[i]->reset_flags();
         es[i]->sync();
       }
-      for (int64_t k = 0; k < steps; ++k) {
-        const bool r = residual && k == steps - 1;
-        // lock step: every slab holds the same buffer parity before sweep k
-        const int par = which == 0 ? es[0]->fc : es[0]->vc;
-        for (int i = 0; i < n; ++i) {
-          lbgpu_engine* e = es[i];
-          CU(cudaSetDevice(e->device));
-          void** nl = which == 0 ? e->nb_left->f : e->nb_left->v;
-          void** nr = which == 0 ? e->nb_right->f : e->nb_right->v;
-          e->push_dst_l = nl[1 - par];
-          e->push_dst_r = nr[1 - par];
-          // neighbours' sweep k-1: their ghosts are read-complete (WAR) and
-          // the planes they pushed into mine are written (RAW)
-          const int prev = int((e->gstep + 1) & 1);
-          CU(cudaStreamWaitEvent(e->st, e->nb_left->ev_step[prev], 0));
-          CU(cudaStreamWaitEvent(e->st, e->nb_right->ev_step[prev], 0));
-          if (which == 0) e->primal_launch(r, nullptr, false);
-          else e->adjoint_launch(kernel, r, nullptr, false);
-          CU(cudaEventRecord(e->ev_step[e->gstep & 1], e->st));
-        }
-        for (int i = 0; i < n; ++i) ++es[i]->gstep;
-      }
+      for (int64_t k = 0; k < steps; ++k) p2p_sweep(es, n, which, kernel, residual && k == steps - 1);
       CU(cudaGetLastError());
       double rmax = 0.0;
       for (int i = 0; i < n; ++i) {
         CU(cudaSetDevice(es[i]->device));
         es[i]->pull_flags();
         if (es[i]->h_flags[1] != kNoBad)
-          es[i]->raise_bad(es[i]->h_flags[1], which == 0 ? "iteration" : "adjoint iteration");
+          es[i]->raise_bad(es[i]->h_flags[1], which == 1 ? "adjoint iteration" : "iteration");
         const double ri = lbgpu_engine::bits_to_double(es[i]->h_flags[0]);
         if (!(ri <= rmax)) rmax = ri;
       }
       if (residual) *residual = rmax;
     });
   }
+  if (which == 2) return LBGPU_E_ARG;  // fused pairs: P2P groups (and single engines) only
   for (int i = 0; i < n; ++i)
     if (!es[i] || (n > 1 && es[i]->xmode != 1)) return LBGPU_E_STATE;
   return guarded(es[0], [&] {
@@ -2155,6 +2238,50 @@ int lbgpu_group_step(lbgpu_engine** es, int n, int which, int64_t steps, int ker
       if (!(ri <= rmax)) rmax = ri;
     }
     if (residual) *residual = rmax;
+  });
+}
+
+// Device time of `steps` lock steps of a P2P group (which as lbgpu_group_step,
+// no residuals): events on every slab's stream around the steps, the maximum
+// over slabs of their elapsed times (each slab ends no earlier than the last
+// neighbour it waited on).
+int lbgpu_group_time(lbgpu_engine** es, int n, int which, int64_t steps, double* ms) {
+  if (!es || n < 2 || steps < 1 || !ms || which < 0 || which > 2) return LBGPU_E_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!es[i] || es[i]->xmode != 3) return LBGPU_E_STATE;
+  if (which == 2 && !es[0]->fuse_pairs()) return LBGPU_E_STATE;
+  return guarded(es[0], [&] {
+    std::vector<cudaEvent_t> t0(n), t1(n);
+    for (int i = 0; i < n; ++i) {
+      CU(cudaSetDevice(es[i]->device));
+      es[i]->reset_flags();
+      es[i]->sync();
+      CU(cudaEventCreate(&t0[i]));
+      CU(cudaEventCreate(&t1[i]));
+    }
+    // one host-side start: every slab's start event is queued before any sweep
+    for (int i = 0; i < n; ++i) {
+      CU(cudaSetDevice(es[i]->device));
+      CU(cudaEventRecord(t0[i], es[i]->st));
+    }
+    for (int64_t k = 0; k < steps; ++k) p2p_sweep(es, n, which, 0, false);
+    double worst = 0.0;
+    for (int i = 0; i < n; ++i) {
+      CU(cudaSetDevice(es[i]->device));
+      CU(cudaEventRecord(t1[i], es[i]->st));
+    }
+    for (int i = 0; i < n; ++i) {
+      CU(cudaSetDevice(es[i]->device));
+      CU(cudaEventSynchronize(t1[i]));
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, t0[i], t1[i]));
+      worst = std::max(worst, double(t));
+      cudaEventDestroy(t0[i]);
+      cudaEventDestroy(t1[i]);
+      es[i]->pull_flags();
+      if (es[i]->h_flags[1] != kNoBad) es[i]->raise_bad(es[i]->h_flags[1], "iteration");
+    }
+    *ms = worst;
   });
 }
 

@@ -172,17 +172,18 @@ constexpr int kHaloPlanes = 6;  // D2Q9+D2Q9: 3+3, D3Q19+D3Q7: 5+1
 template <class L, class R, int D>
 __device__ __forceinline__ void push_halo(const Launch& a, int x, int y, int z, const R* out) {
   const Push& h = a.push;
+  constexpr int F = D == -1 ? 0 : 1;  // the field pulled along D
   const long long row = y + (long long)a.g.ny * z;
-  if (h.r_dst && x == a.g.x1 - 1) {  // my last column -> right neighbour's left ghost
-    R* d = static_cast<R*>(h.r_dst);
+  if (h.r_dst[F] && x == a.g.x1 - 1) {  // my last column -> right neighbour's left ghost
+    R* d = static_cast<R*>(h.r_dst[F]);
     const long long i = (long long)h.r_nx * row + h.r_col;
     LBGPU_FOR(K, 0, kHaloPlanes<L>, {
       constexpr int p = halo_slot<L, D, -1>(K);
       d[p * h.r_N + i] = out[p];
     });
   }
-  if (h.l_dst && x == a.g.x0) {  // my first column -> left neighbour's right ghost
-    R* d = static_cast<R*>(h.l_dst);
+  if (h.l_dst[F] && x == a.g.x0) {  // my first column -> left neighbour's right ghost
+    R* d = static_cast<R*>(h.l_dst[F]);
     const long long i = (long long)h.l_nx * row + h.l_col;
     LBGPU_FOR(K, 0, kHaloPlanes<L>, {
       constexpr int p = halo_slot<L, D, +1>(K);
@@ -1273,8 +1274,10 @@ constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 // FM / VM: addressing of f and v (in place: fsrc == fdst, vsrc == vdst).
 // DUALW: the adjoint half is the previous design's (lbgpu_pair_step_with_design
 // defers each call's adjoint sweep into the next call's fused kernel), so its
-// node constants come from a.t.w_adj while the primal half uses a.t.w.
-template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB, bool DUALW = false>
+// node constants come from a.t.w_adj while the primal half uses a.t.w -- or,
+// GATED, the just-uploaded design value (a.gate; k_pair waits for its slice).
+template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB, bool DUALW = false,
+          bool GATED = false>
 __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fdst,
                                           const R* vsrc, R* vdst, int x, int y, int z, int tid,
                                           unsigned long long& rP, unsigned long long& rA) {
@@ -1305,6 +1308,16 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
   PowPair pp{};
   if (!bb) {
     w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
+    if constexpr (GATED) {
+      const Gate& gt = a.gate;
+      if (x >= gt.bx0 && x < gt.bx1 && y >= gt.by0 && y < gt.by1 && z >= gt.bz0 && z < gt.bz1) {
+        const long long o = (long long)(x - gt.bx0) +
+                            (long long)(gt.bx1 - gt.bx0) *
+                                ((y - gt.by0) + (long long)(gt.by1 - gt.by0) * (z - gt.bz0));
+        w = __ldcg(gt.wd + o);  // landed after this block's flag (L2-coherent load)
+        gt.w_out[idx] = w;
+      }
+    }
     pp = node_pp<false>(a.M, a.t, idx, code, w);
     omt = node_omt<R>(a.M, a.t, code, w);
   }
@@ -1405,18 +1418,33 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
 #define LBGPU_PAIR_BOUNDS(R)                                                   \
   __launch_bounds__(kPairThreads<R>, (sizeof(R) == 4 ? LBGPU_PAIR_MINB32 : LBGPU_PAIR_MINB) * \
                                          128 / kPairThreads<R>)
-template <class L, class R, int CK, bool RESID, bool DUALW = false>
+template <class L, class R, int CK, bool RESID, bool DUALW = false, bool GATED = false>
 __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc,
                                                         R* __restrict__ fdst,
                                                         const R* __restrict__ vsrc,
                                                         R* __restrict__ vdst) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = a.g.z0 + blockIdx.z;
+  if constexpr (GATED) {
+    // the design values of this block's z-plane: wait for the copy engine to
+    // land their slice (blocks start in z order and the upload outruns the
+    // sweep, so only the first planes' blocks ever wait)
+    const Gate& gt = a.gate;
+    if (z >= gt.bz0 && z < gt.bz1) {
+      if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const int c = int((long long)(z - gt.bz0) * gt.slices / (gt.bz1 - gt.bz0));
+        const volatile unsigned* fl = gt.flags + c;
+        while (*fl < gt.seq) __nanosleep(256);
+        __threadfence();
+      }
+      __syncthreads();
+    }
+  }
   unsigned long long rP = 0, rA = 0;
   if (x < a.g.x1 && y < a.g.ny)
-    pair_body<L, R, CK, RESID, FM_DB, FM_DB, DUALW>(a, fsrc, fdst, vsrc, vdst, x, y,
-                                                    a.g.z0 + blockIdx.z,
-                                                    threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
+    pair_body<L, R, CK, RESID, FM_DB, FM_DB, DUALW, GATED>(
+        a, fsrc, fdst, vsrc, vdst, x, y, z, threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
   if constexpr (RESID) {
     detail::block_max_bits(rP, a.fl.resid);
     detail::block_max_bits(rA, a.fl.aux);
@@ -1474,8 +1502,11 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair_aa(Launch a, R* F, R* V, int c0, int
 // — so it carries no dual-number code; design nodes on any other tag (none
 // for config-built cases, config.cpp:355) are the SIDE launch over
 // NodeTables::grad_side with the dual path (design_gradient_node_dual).
+// The analytic kernel stages its v gather through shared memory (cp.async):
+// the loads fly while f is gathered and reduced, and hold no registers, so it
+// fits 4 resident blocks (128 registers) instead of 3 (148).
 template <class L, class R, int AK, bool UPDATE, bool SIDE, int BM = FM_DB, int VM = FM_DB>
-__global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict__ p,
+__global__ void __launch_bounds__(128, (AK == 0 && !SIDE) ? 4 : 1) k_gradient(Launch a, const R* __restrict__ p,
                                                   const R* __restrict__ q,
                                                   const long long* __restrict__ nodes,
                                                   long long n, double* __restrict__ gout,
@@ -1496,16 +1527,22 @@ __global__ void __launch_bounds__(128) k_gradient(Launch a, const R* __restrict_
       const int y = int((idx / g.nx) % g.ny);
       const int z = int(idx / ((long long)g.nx * g.ny));
       const Nbr nb = make_nbr(g, x, y, z);
-      R f[L::M], v[L::M];
-      gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
-      gather_m<L, R, +1, VM>(q, g.N, idx, nb, v);
       const double w = a.t.w[idx];
       const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
       double gv = 0.0;
       bool ok;
       if constexpr (kAnalytic) {
-        ok = design_gradient<L, R>(a.M, pp, f, f + L::MF, R(w), v, v + L::MF, gv);
+        __shared__ R vsm[L::M * 128];
+        R* my = vsm + threadIdx.x;
+        gather_async_m<L, R, +1, VM>(q, g.N, idx, nb, my, 128);
+        R f[L::M];
+        gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
+        cp_async_wait_all();
+        ok = design_gradient<L, R, 128>(a.M, pp, f, f + L::MF, R(w), my, my + L::MF * 128, gv);
       } else {  // design_gradient_node_dual (adjoint.cpp:361-373)
+        R f[L::M], v[L::M];
+        gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
+        gather_m<L, R, +1, VM>(q, g.N, idx, nb, v);
         Dual<R> din[L::M], dout[L::M];
 #pragma unroll
         for (int k = 0; k < L::M; ++k) din[k] = Dual<R>(f[k]);
@@ -1936,7 +1973,10 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
       dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, nzs);
       bool done = false;
       if constexpr (!RES && L::DIM == 3) {
-        if (s.dualw) {
+        if (s.dualw && a.gate.flags) {
+          k_pair<L, R, CK, false, true, true><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
+          done = true;
+        } else if (s.dualw) {
           k_pair<L, R, CK, false, true><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
           done = true;
         }

@@ -498,8 +498,9 @@ LBGPU_HD bool vjp_dual(const Model& M, PowPair pp, int tag, int axis, int sign, 
   return true;
 }
 
-// design_gradient_node (adjoint.cpp:311-358), reference order.
-template <class L, class R>
+// design_gradient_node (adjoint.cpp:311-358), reference order. VS: the stride
+// of vf / vg (1, or the block size when they sit in shared memory).
+template <class L, class R, int VS = 1>
 LBGPU_HD bool design_gradient(const Model& M, PowPair pp, const R* f, const R* g, R w, const R* vf,
                               const R* vg, double& out) {
   R rho, u[3];
@@ -513,7 +514,7 @@ LBGPU_HD bool design_gradient(const Model& M, PowPair pp, const R* f, const R* g
   R Pu[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MF, {
     const R eup = edotp<L, R, J>(up);
-    const R cp = vf[J] * R(L::wf(J)) * rho;
+    const R cp = vf[J * VS] * R(L::wf(J)) * rho;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int ea = L::ef(J, a);
@@ -529,14 +530,14 @@ LBGPU_HD bool design_gradient(const Model& M, PowPair pp, const R* f, const R* g
   therm_eq<L>(temp, up, geq);
   R S[3] = {R(0), R(0), R(0)}, relax = R(0);
   LBGPU_FOR(J, 0, L::MT, {
-    const R c = R(3) * om * temp * vg[J] * R(L::wt(J));
+    const R c = R(3) * om * temp * vg[J * VS] * R(L::wt(J));
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int ea = L::et(J, a);
       if (ea) S[a] = S[a] + (ea > 0 ? c : -c);
       else S[a] = S[a] + c * R(0.0);
     }
-    relax = relax + vg[J] * (geq[J] - g[J]);
+    relax = relax + vg[J * VS] * (geq[J] - g[J]);
   });
   R acc = R(0);
 #pragma unroll

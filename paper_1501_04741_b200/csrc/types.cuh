@@ -38,14 +38,33 @@ struct Flags {
 // P2P halo push targets (in-process slab groups linked with
 // lbgpu_group_link_p2p): the neighbours' destination buffers of this sweep,
 // possibly on other devices (peer memory), and where their ghost columns sit.
+// Index 0 is the primal field's destination, 1 the adjoint field's (a fused
+// pair sweep pushes both).
 struct Push {
-  void* l_dst = nullptr;  // left neighbour: its right ghost column l_col
-  void* r_dst = nullptr;  // right neighbour: its left ghost column r_col
+  void* l_dst[2] = {nullptr, nullptr};  // left neighbour: its right ghost column l_col
+  void* r_dst[2] = {nullptr, nullptr};  // right neighbour: its left ghost column r_col
   int l_col = 0, l_nx = 0, r_col = 0, r_nx = 0;
   long long l_N = 0, r_N = 0;
 };
 
+// Upload-gated design sweep (the deferred design pair's single launch): the
+// design nodes form the box [bx0,bx1) x [by0,by1) x [bz0,bz1) (interior x the
+// design x-range, config.cpp:347-371), whose design values arrive in
+// DesignField::nodes order in wd, in `slices` groups of whole box z-planes,
+// flags[c] reaching `seq` when slice c has landed. A block whose z-plane is
+// in the box waits for its slice, reads its nodes' new w from wd and also
+// writes them into the full-grid design buffer w_out.
+struct Gate {
+  const double* wd = nullptr;
+  double* w_out = nullptr;
+  const unsigned* flags = nullptr;
+  unsigned seq = 0;
+  int slices = 0;
+  int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;
+};
+
 struct Launch {
+  Gate gate;
   Push push;
   Geom g;
   NodeTables t;

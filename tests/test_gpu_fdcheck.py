@@ -8,12 +8,15 @@ re-solve of a 4M-node lattice per FD side is hours of thermal diffusion, so at
 C3 size the check is run on the discrete adjoint of a fixed horizon instead
 (lbgpu_unsteady_adjoint, whose FD partner is fd_gradient with fixed_iters):
 
-* C3 geometry (256x128x128, D3Q19+D3Q7 FMRT) with a uniform inlet
-  temperature, so the mixing objective sum u_n (1 - T^2) is the outflow rate
-  through the support plane -- well conditioned, unlike the split-inlet C3
-  state whose 1 - T^2 is ~1e-9 (test_gpu_fullsize.py);
-* 1,000 developing primal steps, then J = F(f^N) over N = 200 further steps;
-* all 39 FD components (13 x 3 steps x 2 sides, each 200 sweeps from the same
+* C3's lattice (256x128x128, D3Q19+D3Q7 FMRT, mixer3d physics) with a
+  uniform inlet temperature, so the mixing objective sum u_n (1 - T^2) is the
+  outflow rate through the support plane, and a nearly fluid design (w = 0.9
+  +- 0.1) so that there is an outflow to differentiate: C3's own w = 0.5 +- 0.3
+  block (G = w^3 ~ 0.1) throttles the outflow velocity to ~1e-10, where J is
+  ~1e-6, the gradient ~1e-10 and central differences are roundoff (~1e-8);
+* 2,000 developing primal steps, then J = F(f^N) over N = 500 further steps
+  (long enough for the inlet's influence to cross the 256 columns);
+* all 39 FD components (13 x 3 steps x 2 sides, each 500 sweeps from the same
   developed state) through lbgpu_fd_gradient_batch: one call, one host sync.
 """
 import numpy as np
@@ -24,12 +27,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 def test_c3_unsteady_gradient_against_batched_fd(lbgpu, has_gpu):
     from paper_1501_04741_b200.presets import config_text
-    txt = config_text("C3", {"tags.inlet_profile": "uniform", "tags.inlet_T": 0.0})
+    txt = config_text("C3", {"tags.inlet_profile": "uniform", "tags.inlet_T": 0.0,
+                             "optimizer.initial_w": 0.9, "optimizer.init_noise": 0.1})
     e = lbgpu.Engine.from_config(txt)
     e.init_state()
-    e.primal_step(1000, residual=False)
+    e.primal_step(2000, residual=False)
     f_w = e.get_state(0)
-    N = 200
+    N = 500
     J, g, gdp, _ = e.unsteady_adjoint(N, sum_objective=False, slots=16)
     assert J > 0
     e.set_state(0, f_w)
@@ -40,13 +44,15 @@ def test_c3_unsteady_gradient_against_batched_fd(lbgpu, has_gpu):
     hs = steps * (len(order) + 1)
     fd = e.fd_gradient_batch(ords, hs, fixed_iters=N, from_state=True)
     assert np.array_equal(e.get_state(0), f_w)  # state restored
-    worst = 0.0
+    worst, rows = 0.0, []
     for c, o in enumerate(order + [-1]):
         adj = gdp if o < 0 else g[o]
         best = min(abs(fd[3 * c + k] - adj) / max(abs(adj), abs(fd[3 * c + k]), 1e-6 * g_scale)
                    for k in range(3))
+        rows.append((o, adj, list(fd[3 * c: 3 * c + 3]), best))
         worst = max(worst, best)
-    assert worst <= 1e-6, worst
+    assert abs(gdp) > 1e-6 * g_scale, (gdp, g_scale)  # the inlet's influence arrived
+    assert worst <= 1e-5, rows
     e.close()
 
 

@@ -112,3 +112,24 @@ def test_p2p_link_rejects_a_non_group(lbgpu, has_gpu):
     import ctypes as C
     arr = (C.c_void_p * 2)(e.h.value, e.h.value)
     assert lbgpu.load_library().lbgpu_group_link_p2p(arr, 2) == lbgpu.E_ARG
+
+
+@pytest.mark.parametrize("name", ["mix3d", "exch3d", "grad2d", "periodic2d"])
+def test_p2p_group_fused_pairs_equal_monolithic(lbgpu, has_gpu, name):
+    """Fused pair sweeps in the P2P group (each slab's k_pair pushes both
+    fields' cut planes into its neighbours' ghosts): bitwise the monolithic
+    lbgpu_pair_steps; the group timer reports a positive device time."""
+    txt = case_text(name)
+    mono = lbgpu.Engine.from_config(txt)
+    grp = lbgpu.SlabGroup(txt, None, 3, transport="p2p")
+    mono.init_state()
+    grp.init_state()
+    mono.primal_step(12, residual=False)
+    grp.step(0, 12, residual=False)
+    for n in (1, 2, 6):
+        mono.pair_steps(n, residual=False)
+        grp.pair_steps(n)
+        assert np.array_equal(grp.get_state(0), mono.get_state(0))
+        assert np.array_equal(grp.get_state(1), mono.get_state(1))
+    assert grp.time(2, 5) > 0
+

@@ -66,35 +66,39 @@ def full(rep):
 
 
 def main():
+    """ncu_summary.py <launches.csv> <raw.csv[,raw.csv...]> <tag> [launch-list command]"""
     lpath, rep, tag = sys.argv[1:4]
+    cmd = sys.argv[4] if len(sys.argv) > 4 else (
+        "python bench.py --steps 2 --warmup 3 --e2e-steps 2 --no-cpu-baseline")
     table, per = launches(lpath)
     kern = full(rep)
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as fh:
         fh.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
-        fh.write("Command: `python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2`"
-                 " (C3, FP64). Times are cold-cache and serialised: compare shares.\n\n")
+        fh.write(f"Command: `{cmd}` (C3, FP64). Times are cold-cache and serialised: compare "
+                 "shares, not absolutes.\n\n")
         fh.write(table + "\n")
     with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as fh:
-        fh.write(f"# {tag}: ncu --set full (C3 256x128x128, FP64)\n\n"
-                 "One launch per kernel from `bench.py --steps 20 --warmup 3 --no-cpu-baseline "
-                 "--e2e-steps 2` (-s 5 -c 1 each), --clock-control none, cold cache.\n\n")
+        fh.write(f"# {tag}: ncu --set full\n\n"
+                 "One launch per kernel (-c 1 after warm-up launches), --clock-control none, cold "
+                 "cache; targets in tools/probe.py (`ncu pair`: C3 pairs; `ncu gradient`: C4 "
+                 "one-shot; `ncu aa`: C3 in-place pairs).\n\n")
         for d in kern:
             fh.write(f"## {d['kernel']}\n\n")
             for m in METRICS:
                 if m in d:
                     fh.write(f"- {m}: {d[m]}\n")
             fh.write("\n")
-    # traffic per launch (bytes) for bench.py's roofline.traffic
+    # DRAM bytes per launch (bench.py's roofline.traffic reads the k_pair entry)
     tj = {}
     for d in kern:
         def val(m):
             v, u = d[m].split(" ")[0].replace(",", ""), d[m].split(" ")[1] if " " in d[m] else ""
             return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-        key = ("pair_bytes_per_launch" if "k_pair" in d["kernel"] else
-               "adjoint_bytes_per_launch" if "k_adjoint" in d["kernel"] else "primal_bytes_per_launch")
+        name = d["kernel"].split("(")[0].split("<")[0].split()[-1].split("::")[-1]
+        key = "pair_bytes_per_launch" if name == "k_pair" else f"{name}_bytes_per_launch"
         tj[key] = b
-    tj["source"] = f"profiles/{tag}_ncu_full.md (ncu --set full, C3 FP64)"
+    tj["source"] = f"profiles/{tag}_ncu_full.md (ncu --set full)"
     with open(os.path.join(PROF, "traffic.json"), "w") as fh:
         json.dump(tj, fh, indent=1)
     print(table)
