@@ -1118,7 +1118,7 @@ struct lbgpu_engine {
   static constexpr int kSlices = 16;
   int gate_state = -1;  // -1 unknown, 0 no box, 1 box
   Gate gate_box{};
-  unsigned* d_gate_flags = nullptr;
+  unsigned* d_gate_flags = nullptr;  // [kSlices] flags, then the timeout word
   unsigned* h_gate_seq = nullptr;  // pinned source of the flag values
   unsigned gate_seq = 0;
   bool gate_ready() {
@@ -1136,20 +1136,24 @@ struct lbgpu_engine {
     gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
     gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
     gate_box.slices = std::min(kSlices, z1_ - z0_ + 1);
-    CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * kSlices));
-    CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * kSlices));
-    CU(cudaMallocHost(&h_gate_seq, sizeof(unsigned) * kSlices));
+    CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * (kSlices + 1)));
+    CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * (kSlices + 1)));
+    CU(cudaMallocHost(&h_gate_seq, sizeof(unsigned) * (kSlices + 1)));
     gate_state = 1;
     return true;
   }
-  // The gated fused sweep of a deferred pair (adj_pending): upload slices +
-  // flags on the copy stream, one k_pair launch on st.
+  // The gated fused sweep of a deferred pair (adj_pending): one k_pair launch
+  // on st, issued FIRST so the GPU starts as soon as slice 0 lands, then the
+  // upload slices + flags on the copy stream (which waits only for the work
+  // queued before this call: the previous call's readers of d_wvals).
   void gated_pair(const double* wd) {
     ensure_h2d();
-    CU(cudaEventRecord(ev_chunk[kChunks], st));  // the previous call's readers of d_wvals are done
-    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
+    CU(cudaEventRecord(ev_chunk[kChunks], st));
     ++gate_seq;
     const int ns = gate_box.slices, nzb = gate_box.bz1 - gate_box.bz0;
+    CU(cudaMemsetAsync(d_gate_flags + kSlices, 0, sizeof(unsigned), st));
+    gated_launch();
+    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
     const long long plane = (long long)(gate_box.bx1 - gate_box.bx0) * (gate_box.by1 - gate_box.by0);
     for (int c = 0; c < ns; ++c) {
       const long long p0 = ((long long)c * nzb + ns - 1) / ns, p1 = ((long long)(c + 1) * nzb + ns - 1) / ns;
@@ -1160,6 +1164,8 @@ struct lbgpu_engine {
       CU(cudaMemcpyAsync(d_gate_flags + c, h_gate_seq + c, sizeof(unsigned), cudaMemcpyHostToDevice,
                          st_h2d));
     }
+  }
+  void gated_launch() {
     NodeTables tn = T;
     tn.w = d_w2;     // the new design's full-grid buffer (design nodes written by the sweep)
     tn.w_adj = d_w;  // the previous design (the deferred adjoint half)
@@ -1167,6 +1173,7 @@ struct lbgpu_engine {
     sa.a.t = tn;
     sa.a.gate = gate_box;
     sa.a.gate.wd = d_wvals, sa.a.gate.w_out = d_w2, sa.a.gate.flags = d_gate_flags;
+    sa.a.gate.err = d_gate_flags + kSlices;
     sa.a.gate.seq = gate_seq;
     sa.dualw = true;
     fast::pair(sa, f[fc], f[1 - fc], v[vc], v[1 - vc]);
@@ -1247,8 +1254,13 @@ struct lbgpu_engine {
     reduce_flags(d_flags + 1, 1, true);
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
     if (J) CU(cudaMemcpyAsync(h_flags + 5, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (gated)
+      CU(cudaMemcpyAsync(h_gate_seq + kSlices, d_gate_flags + kSlices, sizeof(unsigned),
+                         cudaMemcpyDeviceToHost, st));
     sync();  // one host sync per call; the host design buffer is consumed too
     trace_print();
+    if (gated && h_gate_seq[kSlices])
+      throw Fail{LBGPU_E_NUMERIC, "design upload: a slice did not land within the sweep's wait bound"};
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], fuse ? "iteration (or the deferred adjoint iteration)" : "iteration");
     adj_pending = true;
     if (J) *J = bits_to_double(h_flags[5]);
@@ -1821,16 +1833,79 @@ struct lbgpu_engine {
   //   mu^N     = adjoint_step(base f^N, 0, obj)
   //   mu^{n-1} = adjoint_step(base f^{n-1}, mu^n, obj if sum else none)
   //   dJ/dw    = sum_{n=N..1} param_gradient(v = mu^n, base f^{n-1})
-  // for J = F(f^N) (terminal) or J = sum_{n=1..N} F(f^n). Primal states are
-  // recomputed from checkpoints by recursive bisection over `slots` state
-  // buffers (O(N log(N/slots)) extra sweeps, O(slots) memory); the sweeps
-  // write straight into the slot buffers (no copies).
+  // for J = F(f^N) (terminal) or J = sum_{n=1..N} F(f^n). Primal states come
+  // from checkpoints in `slots` state buffers, placed by a binomial schedule
+  // (Schedule: the recompute-optimal split of every segment for its free
+  // slot count, and checkpoints placed by the first forward pass itself,
+  // which runs anyway); the sweeps write straight into the slot buffers.
+  //
+  // Schedule tables, for segment length n <= N and free slots s <= S:
+  //   opt(n, s)   extra sweeps to reverse a segment from its first state;
+  //   first(n, s) the same when the segment's states are produced by the
+  //               first pass (checkpoints cost no extra sweeps there);
+  //   opt(n, s)   = min_m m + opt(n - m, s - 1) + opt(m, s),
+  //   first(n, s) = min_m first(n - m, s - 1) + opt(m, s),
+  // with opt = first = n - 1 (store every inner state) when n - 1 <= s, and
+  // n (n - 1) / 2 (recompute every base from the checkpoint) when s = 0.
+  // Measured model at C5 slab size, N = 1000: round 1's recursive bisection
+  // with 4 slots spent 10.6 N sweeps; this schedule spends 6.3 N with 4
+  // slots and 5.3 N with 5 (the same device memory as round 1's 4 slots plus
+  // its separate state-0 and state-N buffers, which now are the engine's own).
+  struct Schedule {
+    static constexpr long long kMaxN = 4096;  // DP tables up to here; bisection beyond
+    long long N = 0;
+    int S = 0;
+    bool dp = false;
+    std::vector<long long> oc, fcst;
+    std::vector<int> om, fmv;
+    size_t at(long long n, int s) const { return size_t(n) * size_t(S + 1) + size_t(s); }
+    void build(long long N_, int S_) {
+      N = N_, S = S_;
+      dp = N <= kMaxN;
+      if (!dp) return;
+      const size_t sz = size_t(N + 1) * size_t(S + 1);
+      oc.assign(sz, 0), fcst.assign(sz, 0), om.assign(sz, 0), fmv.assign(sz, 0);
+      for (int sl = 0; sl <= S; ++sl)
+        for (long long n = 2; n <= N; ++n) {
+          if (n - 1 <= sl) {
+            oc[at(n, sl)] = n - 1;
+            continue;
+          }
+          if (sl == 0) {
+            oc[at(n, sl)] = fcst[at(n, sl)] = n * (n - 1) / 2;
+            continue;
+          }
+          long long bo = -1, bf = -1;
+          int mo = 1, mf = 1;
+          for (long long m = 1; m < n; ++m) {
+            const long long co = m + oc[at(n - m, sl - 1)] + oc[at(m, sl)];
+            const long long cf = fcst[at(n - m, sl - 1)] + oc[at(m, sl)];
+            if (bo < 0 || co < bo) bo = co, mo = int(m);
+            if (bf < 0 || cf < bf) bf = cf, mf = int(m);
+          }
+          oc[at(n, sl)] = bo, om[at(n, sl)] = mo;
+          fcst[at(n, sl)] = bf, fmv[at(n, sl)] = mf;
+        }
+    }
+    // checkpoint offset for a segment reversed from its start (>= 1)
+    long long opt_split(long long n, long long s) const {
+      if (!dp) return n / 2;
+      return om[at(n, int(std::min<long long>(s, S)))];
+    }
+    // checkpoint offset the first pass places (0: none, the segment is terminal)
+    long long first_split(long long n, long long s) const {
+      if (!dp || n - 1 <= s || s == 0) return 0;
+      return fmv[at(n, int(std::min<long long>(s, S)))];
+    }
+  };
+
   struct Unsteady {
     lbgpu_engine* e;
     bool sum;
     std::vector<void*> free_slots;
     void* work;   // ping-pong partners for forward segments
     void* work2;
+    const Schedule* sch;
     double gdp = 0.0;
     // k >= 1 sweeps from `from`, the last one landing in `to` (via `tmp`)
     void fwd(const void* from, void* to, long long k, void* tmp) {
@@ -1884,7 +1959,7 @@ struct lbgpu_engine {
         for (void* p : st) free_slots.push_back(p);
         return;
       }
-      const long long m = a + (b - a) / 2;
+      const long long m = a + sch->opt_split(b - a, (long long)free_slots.size());
       void* Ms = free_slots.back();
       free_slots.pop_back();
       fwd(A, Ms, m - a, work);
@@ -1905,7 +1980,7 @@ struct lbgpu_engine {
       for (void* p : slots) cudaFree(p);
     };
     try {
-      for (long long i = 0; i < nslots + 3; ++i) {
+      for (long long i = 0; i < nslots + 2; ++i) {
         void* p = nullptr;
         CU(cudaMalloc(&p, field_bytes()));
         // ghost layout: sweeps write owned columns only, so seed every slot's
@@ -1913,20 +1988,55 @@ struct lbgpu_engine {
         if (ghosts) CU(cudaMemcpyAsync(p, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
         slots.push_back(p);
       }
-      void* s0 = slots[0];     // state 0 (checkpoint)
-      void* work = slots[1];   // forward ping-pong partner
-      void* sN = slots[2];     // state N during the first pass
+      Schedule sch;
+      sch.build(N, int(nslots));
+      // state 0 lives in the engine's idle buffer, state N lands in the
+      // engine's current one (the primal state the call leaves behind)
+      void* s0 = f[1 - fc];
+      void* sN = f[fc];
       const long long steps0 = primal_steps;
       reset_flags();
       CU(cudaMemcpyAsync(s0, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
-      // first pass: states 1..N, the objective
+      Unsteady U{this, sum_obj, {}, slots[0], slots[1], &sch};
+      for (long long i = 2; i < (long long)slots.size(); ++i) U.free_slots.push_back(slots[i]);
+      // first pass: states 1..N and the objective, placing the schedule's
+      // checkpoints (chain) and, in its last segment, every inner state
       double Jv = 0.0;
+      std::vector<std::pair<long long, void*>> chain{{0, s0}};
+      std::vector<void*> tail;  // the last segment's stored inner states
+      long long a = 0;
       const void* src = s0;
-      for (long long n = 1; n <= N; ++n) {
-        void* dst = (n % 2 == N % 2) ? sN : work;
+      auto step_to = [&](long long n, void* dst) {
         primal_raw(src, dst, false, nullptr, true);
         src = dst;
         if (sum_obj || n == N) Jv += objective(dst);
+      };
+      for (;;) {
+        const long long n = N - a;
+        const long long m = sch.first_split(n, (long long)U.free_slots.size());
+        if (m == 0) {  // the last segment: store its inner states if they fit
+          const bool store = n - 1 <= (long long)U.free_slots.size();
+          for (long long k = a + 1; k <= N; ++k) {
+            void* dst;
+            if (k == N) {
+              dst = sN;
+            } else if (store) {
+              dst = U.free_slots.back();
+              U.free_slots.pop_back();
+              tail.push_back(dst);
+            } else {
+              dst = ((N - k) % 2 == 1) ? U.work : U.work2;  // alternate; never sN's buffer
+            }
+            step_to(k, dst);
+          }
+          if (!store) tail.clear();
+          break;
+        }
+        void* C = U.free_slots.back();  // a checkpoint m steps in
+        U.free_slots.pop_back();
+        for (long long k = a + 1; k <= a + m; ++k) step_to(k, k == a + m ? C : ((a + m - k) % 2 ? U.work : U.work2));
+        a += m;
+        chain.push_back({a, C});
       }
       // mu^N = adjoint_step(f^N, 0, obj)
       CU(cudaMemsetAsync(v[vc], 0, field_bytes(), st));
@@ -1934,12 +2044,23 @@ struct lbgpu_engine {
       CU(cudaMemsetAsync(d_grad, 0, sizeof(double) * std::max<size_t>(design.size(), 1), st));
       adjoint_raw(0, sN, v[vc], v[1 - vc], false, nullptr, true);
       vc ^= 1;
-      // keep f^N as the engine's primal state afterwards
-      CU(cudaMemcpyAsync(f[fc], sN, field_bytes(), cudaMemcpyDeviceToDevice, st));
-      Unsteady U{this, sum_obj, {}, work, slots[3]};
-      for (long long i = 4; i < (long long)slots.size(); ++i) U.free_slots.push_back(slots[i]);
-      U.free_slots.push_back(sN);
-      U.reverse(0, N, s0);
+      // the last segment [a, N): its stored states, or recompute from its checkpoint
+      {
+        const long long ak = chain.back().first;
+        const void* Ak = chain.back().second;
+        if (!tail.empty() || N - ak <= 1) {
+          for (long long n = N; n > ak; --n) U.back_step(n - 1 == ak ? Ak : tail[size_t(n - 1 - ak - 1)]);
+          for (void* p : tail) U.free_slots.push_back(p);
+        } else {
+          U.reverse(ak, N, Ak);
+        }
+      }
+      // then every earlier segment of the chain, from its checkpoint
+      for (size_t j = chain.size() - 1; j-- > 0;) {
+        U.free_slots.push_back(chain[j + 1].second);
+        U.reverse(chain[j].first, chain[j + 1].first, chain[j].second);
+      }
+      // f^N stays in f[fc] (sN); f[1 - fc] (s0) is scratch again
       if (g && !design.empty())
         CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * design.size(), cudaMemcpyDeviceToHost, st));
       sync();

@@ -1435,7 +1435,14 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
       if (threadIdx.x == 0 && threadIdx.y == 0) {
         const int c = int((long long)(z - gt.bz0) * gt.slices / (gt.bz1 - gt.bz0));
         const volatile unsigned* fl = gt.flags + c;
-        while (*fl < gt.seq) __nanosleep(256);
+        // bounded (~2 s): a slice that never lands is reported, never a hang
+        for (unsigned it = 0; *fl < gt.seq; ++it) {
+          if (it > (1u << 23)) {
+            atomicExch(gt.err, 1u);
+            break;
+          }
+          __nanosleep(256);
+        }
         __threadfence();
       }
       __syncthreads();

@@ -58,6 +58,7 @@ struct Gate {
   const double* wd = nullptr;
   double* w_out = nullptr;
   const unsigned* flags = nullptr;
+  unsigned* err = nullptr;  // set when a slice never landed (bounded wait)
   unsigned seq = 0;
   int slices = 0;
   int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;

@@ -18,6 +18,12 @@ C3 size the check is run on the discrete adjoint of a fixed horizon instead
   (long enough for the inlet's influence to cross the 256 columns);
 * all 39 FD components (13 x 3 steps x 2 sides, each 500 sweeps from the same
   developed state) through lbgpu_fd_gradient_batch: one call, one host sync.
+
+grad_check's error rule, best of the reference's steps {1e-5, 1e-6, 1e-7}, at
+1e-4: here J is the outflow through 15,876 support nodes (~1e2), so central
+differences carry ~1e-16 J / h of roundoff (1e-4 relative at h = 1e-6 for
+these ~1e-4 components) and h = 1e-5 leaves a ~1e-5 truncation error after
+500 steps (measured: the worst component agrees to 3.4e-5).
 """
 import numpy as np
 import pytest
@@ -52,7 +58,7 @@ def test_c3_unsteady_gradient_against_batched_fd(lbgpu, has_gpu):
         rows.append((o, adj, list(fd[3 * c: 3 * c + 3]), best))
         worst = max(worst, best)
     assert abs(gdp) > 1e-6 * g_scale, (gdp, g_scale)  # the inlet's influence arrived
-    assert worst <= 1e-5, rows
+    assert worst <= 1e-4, rows
     e.close()
 
 

@@ -17,8 +17,13 @@ compiled from its own sources) on identical inputs at full size:
   design iterations compared (C2: 50; C4: 20 at 128x32x32 and 3 at full size).
 * C5 (D3Q19 mixer physics): the unsteady adjoint of N_t = 200 cold-start steps
   at 128x32x32 against the composition of the reference's own operators
-  (SURVEY.md §8a A14 recipe), pinned by the reference's fd_gradient(fixed_iters
-  = N_t) on 3 design nodes.
+  (SURVEY.md §8a A14 recipe), bitwise in the exact build. At this state the
+  gradient is ~1e-16 (the porous block w ~ 0.5 has not let any flow reach the
+  support plane), below what central differences resolve, so the FD pin --
+  fd_gradient(fixed_iters = N_t) on the 3 strongest design nodes (bitwise the
+  reference's in the exact build, test_gpu_fdcheck.py) -- runs on the same
+  lattice with a nearly fluid design (w = 0.9 +- 0.1), uniform inlet and
+  N_t = 400, where the flow crosses the channel.
 
 Tolerances are SURVEY.md §8(d)'s (FP64): state <= 1e-12 of max|f| (adjoint
 state <= 1e-11 of max|v|, see test_gpu_parity.py); design gradient <= 1e-10
@@ -264,21 +269,21 @@ def test_c5_unsteady_adjoint_protocol(lbgpu, oracle_mod, has_gpu):
             assert abs(gdp - gdp_r) <= max(GRAD_RTOL * abs(gdp_r), 10 * abs(gdp_p - gdp_r))
         e.close()
     # fd_gradient(fixed_iters = N) (adjoint.cpp:492-517) on the 3 strongest
-    # design components, the reference's step set and error rule
-    # (case.cpp:256-283); the first one by the reference itself, all three by
-    # the bit-exact engine (equal to the reference's fd_gradient bit for bit)
-    order = np.argsort(-np.abs(g_r), kind="stable")[:3]
-    r = oracle_mod.RefOracle(txt)
-    x = lbgpu.Engine.from_config(txt, exact=True)
+    # design components with the reference's step set and error rule
+    # (case.cpp:256-283), in the bit-exact build, on the well-conditioned variant
+    N2 = 400
+    txt2 = cfg("C5", {**C5_SMALL, "optimizer.initial_w": 0.9, "optimizer.init_noise": 0.1,
+                      "tags.inlet_profile": "uniform", "tags.inlet_T": 0.0})
+    x = lbgpu.Engine.from_config(txt2, exact=True)
     x.init_state()
+    J2, g2, gdp2, _ = x.unsteady_adjoint(N2, sum_objective=False, slots=8)
+    gs2 = max(np.max(np.abs(g2)), abs(gdp2))
+    x.init_state()
+    order = [int(o) for o in np.argsort(-np.abs(g2), kind="stable")[:3]]
+    hs = [1e-5, 1e-6, 1e-7]
+    fd = x.fd_gradient_batch([o for o in order for _ in hs], hs * 3, fixed_iters=N2)
     for k, o in enumerate(order):
-        best = np.inf
-        for h in (1e-5, 1e-6, 1e-7):
-            fd = x.fd_gradient(int(o), h, 0.0, N, fixed_iters=N)
-            if k == 0 and h == 1e-6:
-                assert fd == r.fd_gradient(int(o), h, 0.0, N, N)
-            den = max(abs(g_r[o]), abs(fd), 1e-6 * gs, 1e-300)
-            best = min(best, abs(fd - g_r[o]) / den)
-        assert best <= 1e-4, (int(o), best)
+        best = min(abs(fd[3 * k + j] - g2[o]) / max(abs(g2[o]), abs(fd[3 * k + j]), 1e-6 * gs2)
+                   for j in range(3))
+        assert best <= 1e-4, (o, g2[o], list(fd[3 * k: 3 * k + 3]), best)
     x.close()
-    r.close()
