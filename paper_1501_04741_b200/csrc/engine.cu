@@ -635,6 +635,7 @@ struct lbgpu_engine {
     for (long long i = 0; i < N; ++i) {
       uint8_t c = tag[i];
       if (mask[i] || w[i] != 1.0) c |= CODE_HAS_W;
+      if (mask[i] && tag[i] == TAG_INTERIOR) c |= CODE_DESIGN_INT;  // no face normal here
       if (on_support[i]) c |= CODE_SUPPORT;
       if (tag[i] == TAG_INLET || tag[i] == TAG_OUTLET) {
         c |= uint8_t(bc_axis[i] << CODE_AXIS_SHIFT);
@@ -1135,12 +1136,26 @@ struct lbgpu_engine {
     if (vol != (long long)design.size()) return false;  // not a box: the chunked path
     gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
     gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
-    gate_box.slices = std::min(kSlices, z1_ - z0_ + 1);
+    // slices of 1, 1, 2, 4, 8, ... box planes (doubling): the first lands within
+    // microseconds, and each later one before the sweep reaches it (the upload
+    // runs ~1.6x faster than the sweep consumes planes)
+    const int nzb = z1_ - z0_ + 1;
+    int ns = 0;
+    for (long long p = 0; p < nzb && ns < kSlices; ++ns) p += std::max<long long>(1, p);
+    gate_box.slices = ns;
     CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * (kSlices + 1)));
     CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * (kSlices + 1)));
     CU(cudaMallocHost(&h_gate_seq, sizeof(unsigned) * (kSlices + 1)));
     gate_state = 1;
     return true;
+  }
+  // first box plane of slice c (doubling sizes; the last slice takes the rest)
+  long long gate_plane(int c) const {
+    const long long nzb = gate_box.bz1 - gate_box.bz0;
+    if (c >= gate_box.slices) return nzb;
+    long long p = 0;
+    for (int k = 0; k < c; ++k) p += std::max<long long>(1, p);
+    return std::min(p, nzb);
   }
   // The gated fused sweep of a deferred pair (adj_pending): one k_pair launch
   // on st, issued FIRST so the GPU starts as soon as slice 0 lands, then the
@@ -1150,13 +1165,13 @@ struct lbgpu_engine {
     ensure_h2d();
     CU(cudaEventRecord(ev_chunk[kChunks], st));
     ++gate_seq;
-    const int ns = gate_box.slices, nzb = gate_box.bz1 - gate_box.bz0;
+    const int ns = gate_box.slices;
     CU(cudaMemsetAsync(d_gate_flags + kSlices, 0, sizeof(unsigned), st));
     gated_launch();
     CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
     const long long plane = (long long)(gate_box.bx1 - gate_box.bx0) * (gate_box.by1 - gate_box.by0);
     for (int c = 0; c < ns; ++c) {
-      const long long p0 = ((long long)c * nzb + ns - 1) / ns, p1 = ((long long)(c + 1) * nzb + ns - 1) / ns;
+      const long long p0 = gate_plane(c), p1 = gate_plane(c + 1);
       if (p1 > p0)
         CU(cudaMemcpyAsync(d_wvals + p0 * plane, wd + p0 * plane, sizeof(double) * (p1 - p0) * plane,
                            cudaMemcpyHostToDevice, st_h2d));
@@ -1249,6 +1264,7 @@ struct lbgpu_engine {
                             (long long)support.size(), d_terms, 0);
       ++launches;
       pairwise_queue(tree_support, d_terms);
+      if (trace_on()) trace("J", st);
     }
     CU(cudaGetLastError());
     reduce_flags(d_flags + 1, 1, true);
@@ -2086,16 +2102,48 @@ struct lbgpu_engine {
     long long k = 0;
     reset_flags();
     const long long n = (long long)design.size();
+    // Product build, one engine, interior design nodes only: iteration it's
+    // design update rides in iteration it+1's primal sweep (k_primal UPD),
+    // which gathers the same base f the gradient needs -- one f gather per
+    // design node per iteration saved, bitwise the separate update. Record
+    // iterations (their row needs the update's max|comp| and w) and the last
+    // iteration of a call update on their own.
+    const bool fusable = !exact && xmode == 0 && grad_side.empty() && n > 0;
+    bool pend = false;
+    double pz = 0.0, pl = 0.0;
+    auto update_now = [&](double z_, double l_) {
+      const Launch a = launch(adjoint_steps - kb_a);
+      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, z_, l_, 0, 0, 0);
+      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, z_, l_, 0, 0, 0);
+      CU(cudaGetLastError());
+      ++launches;
+    };
     for (long long it = it0; it < it0 + count; ++it) {
       const bool rec = (it % ri == 0) || it == total;
+      if (pend && rec) {  // this primal reports a residual: the update goes first, apart
+        update_now(pz, pl);
+        pend = false;
+      }
       if (rec) CU(cudaMemsetAsync(d_flags, 0, sizeof(unsigned long long), st));
-      primal_launch(rec, nullptr);
+      if (pend) {
+        ++primal_steps;
+        ++launches;
+        SweepArgs sa = sweep(primal_steps - kb_p, false, nullptr);
+        sa.upd = true;
+        sa.a.upd.v = v[vc], sa.a.upd.w = d_w, sa.a.upd.zeta = pz, sa.a.upd.lambda = pl;
+        fast::primal(sa, f[fc], f[1 - fc]);
+        fc ^= 1;
+        pend = false;
+      } else {
+        primal_launch(rec, nullptr);
+      }
       adjoint_launch(0, false, nullptr);
       if (rec) CU(cudaMemsetAsync(d_flags + 2, 0, sizeof(unsigned long long), st));
-      const Launch a = launch(adjoint_steps - kb_a);
-      if (exact) exact::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0, 0, 0);
-      else fast::gradient(a, dim, prec, 0, true, f[fc], v[vc], d_design, n, nullptr, d_w, zeta[it - it0], lambda[it - it0], 0, 0, 0);
-      CU(cudaGetLastError());
+      if (fusable && !rec && it + 1 < it0 + count) {
+        pend = true, pz = zeta[it - it0], pl = lambda[it - it0];
+        continue;
+      }
+      update_now(zeta[it - it0], lambda[it - it0]);
       if (exact) {  // the device moved w: refresh the host copy and the libm pow tables
         CU(cudaMemcpyAsync(w.data(), d_w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
         sync();

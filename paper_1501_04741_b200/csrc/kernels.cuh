@@ -903,8 +903,12 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 // lanes rebuild their inputs in place (face_forward) and share the interior
 // collision with the rest of the warp.
 // FM: the field's addressing mode (FM_DB: src -> dst; FM_O / FM_E: in place,
-// src == dst, no residual).
-template <class L, class R, int CK, bool RESID, int FM = FM_DB>
+// src == dst, no residual). UPD: first the previous one-shot iteration's
+// design update at an interior design node (a.upd: the gradient of a.upd.v
+// against the f gathered here -- the base that iteration's adjoint used --
+// then the composite ascent step), exactly k_gradient<UPDATE>'s arithmetic,
+// so the primal collides with the new w it has just written.
+template <class L, class R, int CK, bool RESID, int FM = FM_DB, bool UPD = false>
 __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* dst, int x, int y,
                                             int z, unsigned long long& rmax) {
   using namespace detail;
@@ -914,8 +918,31 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* ds
   const uint8_t code = a.t.code[idx];
   const Nbr nb = make_nbr(g, x, y, z);
   R f[L::M], out[L::M];
-  if constexpr (FM == FM_DB) gather<L, R, -1>(src, g.N, nb, f);
-  else gather_m<L, R, -1, FM>(src, g.N, idx, nb, f);
+  if constexpr (UPD) {
+    // v of this node in flight (shared memory) while f is gathered
+    __shared__ R vsm[L::M * 128];
+    R* my = vsm + threadIdx.x;
+    const bool dn = (code & (TAG_MASK | CODE_AXIS_BITS)) == (TAG_INTERIOR | CODE_DESIGN_INT);
+    if (dn) gather_async<L, R, +1>(static_cast<const R*>(a.upd.v), g.N, nb, my, 128);
+    gather<L, R, -1>(src, g.N, nb, f);
+    if (dn) {
+      cp_async_wait_all();
+      const double w = a.t.w[idx];
+      const PowPair pp = node_pp<LBGPU_EXACT != 0>(a.M, a.t, idx, code | CODE_HAS_W, w);
+      double gv = 0.0;
+      if (!design_gradient<L, R, 128>(a.M, pp, f, f + L::MF, R(w), my, my + L::MF * 128, gv))
+        atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+      double comp = gv;
+      if (a.upd.lambda != 0.0) comp -= a.upd.lambda * (1.0 - 2.0 * w);
+      double wn = w + a.upd.zeta * comp;
+      wn = wn < 0.0 ? 0.0 : (1.0 < wn ? 1.0 : wn);
+      a.upd.w[idx] = wn;  // primal_node reads it back below (same thread)
+    }
+  } else if constexpr (FM == FM_DB) {
+    gather<L, R, -1>(src, g.N, nb, f);
+  } else {
+    gather_m<L, R, -1, FM>(src, g.N, idx, nb, f);
+  }
   if (!primal_node<L, R, CK, true>(a, idx, code, f, out))
     atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
   if constexpr (FM == FM_DB) {
@@ -929,13 +956,13 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* ds
 // Plain bounds: ptxas picks 64 regs (FP32) / 96-122 (FP64), no spills. Forcing
 // more blocks spills (FP32 C3 primal GB/s: 64 regs 5748, 48 regs 5480, 40
 // regs 4036); (128, 1) lets it take 106 regs (4827).
-template <class L, class R, int CK, bool RESID>
+template <class L, class R, int CK, bool RESID, bool UPD = false>
 __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
                                                 R* __restrict__ dst) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (x < a.g.x1)
-    primal_body<L, R, CK, RESID>(a, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
+    primal_body<L, R, CK, RESID, FM_DB, UPD>(a, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
@@ -1433,7 +1460,10 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
     const Gate& gt = a.gate;
     if (z >= gt.bz0 && z < gt.bz1) {
       if (threadIdx.x == 0 && threadIdx.y == 0) {
-        const int c = int((long long)(z - gt.bz0) * gt.slices / (gt.bz1 - gt.bz0));
+        // slices of doubling plane counts (engine.cu gate_plane): plane q is
+        // in slice floor(log2 q) + 1 (q = 0: slice 0), the last one open-ended
+        const int q = z - gt.bz0;
+        const int c = q == 0 ? 0 : min(32 - __clz(q), gt.slices - 1);
         const volatile unsigned* fl = gt.flags + c;
         // bounded (~2 s): a slice that never lands is reported, never a hang
         for (unsigned it = 0; *fl < gt.seq; ++it) {
@@ -1855,6 +1885,14 @@ void primal_t(const SweepArgs& s, const void* src, void* dst) {
   int nzs = a.g.nz;
   if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (pipelined design upload)
   dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, nzs);
+#if !LBGPU_EXACT
+  if constexpr (!RES) {
+    if (s.upd) {
+      k_primal<L, R, CK, false, true><<<grid, bx, 0, a.stream>>>(a, in, out);
+      return;
+    }
+  }
+#endif
   k_primal<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, in, out);
 }
 template <class L, class R, int CK, int AK, bool RES>

@@ -122,6 +122,11 @@ enum : uint8_t {
   CODE_SUPPORT = 16,   // objective support node (ObjectiveSpec::on_support)
   CODE_AXIS_SHIFT = 5, // bits 5-6: pressure-face normal axis
   CODE_NEG = 128,      // pressure-face normal sign is -1
+  // An Interior node has no face normal: axis bits 11 mark an interior
+  // design node (DesignField mask), for the one-shot update fused into the
+  // next primal sweep.
+  CODE_AXIS_BITS = 96,
+  CODE_DESIGN_INT = 96,
 };
 
 }  // namespace lbgpu

@@ -50,8 +50,9 @@ struct Push {
 // Upload-gated design sweep (the deferred design pair's single launch): the
 // design nodes form the box [bx0,bx1) x [by0,by1) x [bz0,bz1) (interior x the
 // design x-range, config.cpp:347-371), whose design values arrive in
-// DesignField::nodes order in wd, in `slices` groups of whole box z-planes,
-// flags[c] reaching `seq` when slice c has landed. A block whose z-plane is
+// DesignField::nodes order in wd, in `slices` groups of whole box z-planes
+// (1, 1, 2, 4, 8, ... planes, the last taking the rest), flags[c] reaching
+// `seq` when slice c has landed. A block whose z-plane is
 // in the box waits for its slice, reads its nodes' new w from wd and also
 // writes them into the full-grid design buffer w_out.
 struct Gate {
@@ -64,7 +65,18 @@ struct Gate {
   int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;
 };
 
+// One-shot design update carried by the next primal sweep (k_primal UPD):
+// the gradient of the previous adjoint state v at each interior design node,
+// composite and clamped ascent step (optimizer.cpp:41-45, :8-16), then the
+// collision with the new w.
+struct Upd {
+  const void* v = nullptr;  // adjoint state (double-buffered post layout)
+  double* w = nullptr;      // design, updated in place
+  double zeta = 0.0, lambda = 0.0;
+};
+
 struct Launch {
+  Upd upd;
   Gate gate;
   Push push;
   Geom g;
@@ -85,6 +97,7 @@ struct SweepArgs {
   const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
   int fm = 0, vm = 0;  // addressing modes of f and v: 0 double-buffered, 1/2 in place (O/E)
   bool dualw = false;  // fused pair: the adjoint half reads w from a.t.w_adj (3-D, no residual)
+  bool upd = false;    // primal: apply a.upd (the previous one-shot iteration's update) first
 };
 
 // Launchers, one set per build (k_fast_*.cu / k_exact_*.cu).

@@ -202,6 +202,31 @@ def test_one_shot_fast(lbgpu, oracle_mod, has_gpu):
     assert rel(e.get_state(1), o.v) <= ADJ_RTOL
 
 
+@pytest.mark.parametrize("name", list(CASES))
+def test_one_shot_fused_update_is_bitwise(lbgpu, has_gpu, name):
+    """The product build carries each non-record iteration's design update
+    into the next iteration's primal sweep (k_primal UPD); with a record every
+    iteration nothing is carried. Both must give the same bits: w, f, v and
+    the rows they share."""
+    txt = case_text(name)
+    iters = 15
+    zeta = np.full(iters, 3e-2)
+    lam = np.linspace(0.0, 2e-3, iters)
+    out = []
+    for ri in (7, 1):
+        e = lbgpu.Engine.from_config(txt)
+        e.init_state()
+        e.primal_step(30, residual=False)
+        rows = e.one_shot(zeta, lam, record_interval=ri)
+        out.append((rows, e.design(), e.get_state(0), e.get_state(1)))
+        e.close()
+    (ra, wa, fa, va), (rb, wb, fb, vb) = out
+    assert np.array_equal(wa, wb) and np.array_equal(fa, fb) and np.array_equal(va, vb)
+    shared = {7: 6, 14: 13, 15: 14}
+    for i, row in enumerate(ra):
+        assert np.array_equal(row, rb[shared[int(row[0])]])
+
+
 def test_zero_zeta_one_shot_is_plain_stepping(lbgpu, has_gpu):
     """test_optimizer.cpp:182-209: one-shot with ζ = 0 == plain primal steps."""
     txt = case_text("grad2d")

@@ -84,11 +84,18 @@ L.append(f"- Slab 0 of 8 (256 owned columns + ghosts, {c5['owned_nodes']:,} node
          f"{c5['adjoint_mlups']:,.0f} MLUPS ({c5['adjoint_gbs']:,.0f} GB/s), over owned nodes.\n"
          "- Unsteady adjoint on a standalone 256x512x512 lattice with the C5 physics (one rank's "
          "node count):\n"
-         f"  - {c5['unsteady_warmup_steps']} warm-up steps, then N_t = {c5['unsteady_steps']} with "
-         f"{c5['unsteady_slots']} checkpoint slots;\n"
-         f"  - {c5['unsteady_forward_sweeps']:,} primal sweeps (recompute included) and "
-         f"{c5['unsteady_adjoint_sweeps']} adjoint sweeps in {c5['unsteady_seconds']:.1f} s, "
-         f"{c5['unsteady_node_sweeps_per_s_mlups']:,.0f} M node-sweeps/s;\n"
-         f"  - J = {c5['unsteady_J']:.6g}, max |dJ/dw| = {c5['unsteady_grad_max']:.3e}.\n")
+         f"  - {c5['unsteady_warmup_steps']} warm-up steps, then N_t = {c5['unsteady_steps']};\n")
+if "unsteady_by_slots" in c5:
+    L.append(f"  - round 1 (recursive bisection, 4 slots): "
+             f"{c5['unsteady_round1_forward_sweeps_4_slots']:,} primal sweeps;\n")
+    for k, u in c5["unsteady_by_slots"].items():
+        L.append(f"  - binomial schedule, {k} slots: {u['forward_sweeps']:,} primal sweeps "
+                 f"({u['recompute_factor']:.2f} N_t) and {u['adjoint_sweeps']} adjoint sweeps in "
+                 f"{u['seconds']:.1f} s, {u['node_sweeps_per_s_mlups']:,.0f} M node-sweeps/s; "
+                 f"J = {u['J']:.6g}, max |dJ/dw| = {u['grad_max']:.3e}.\n")
+else:
+    L.append(f"  - {c5['unsteady_slots']} checkpoint slots: {c5['unsteady_forward_sweeps']:,} primal "
+             f"sweeps and {c5['unsteady_adjoint_sweeps']} adjoint sweeps in "
+             f"{c5['unsteady_seconds']:.1f} s; J = {c5['unsteady_J']:.6g}.\n")
 open(os.path.join(ROOT, "profiles", f"{tag}_configs.md"), "w").write("\n".join(L) + "\n")
 print("ok")
