@@ -1116,7 +1116,7 @@ struct lbgpu_engine {
   // fused sweep of a deferred pair is ONE launch whose blocks wait on
   // per-slice flags the copy engine sets behind each slice of the upload --
   // no z-chunk kernel boundaries, no scatter kernels.
-  static constexpr int kSlices = 16;
+  static constexpr int kSlices = 24;
   int gate_state = -1;  // -1 unknown, 0 no box, 1 box
   Gate gate_box{};
   unsigned* d_gate_flags = nullptr;  // [kSlices] flags, then the timeout word
@@ -1136,12 +1136,15 @@ struct lbgpu_engine {
     if (vol != (long long)design.size()) return false;  // not a box: the chunked path
     gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
     gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
-    // slices of 1, 1, 2, 4, 8, ... box planes (doubling): the first lands within
-    // microseconds, and each later one before the sweep reaches it (the upload
-    // runs ~1.6x faster than the sweep consumes planes)
+    // slices of 1, 2, 3, 4, 6 box planes, then 8 each: the first lands within
+    // microseconds, and every later one before the sweep reaches its first
+    // plane (the upload moves ~1.6 planes per plane the sweep finishes, so a
+    // slice [a, b) is never waited for once b / a < 1.6; measured: equal
+    // 8-plane slices wait ~25 us for the first, doubling sizes wait on the
+    // large last ones)
     const int nzb = z1_ - z0_ + 1;
     int ns = 0;
-    for (long long p = 0; p < nzb && ns < kSlices; ++ns) p += std::max<long long>(1, p);
+    for (long long p = 0; p < nzb && ns < kSlices - 1; ++ns) p = gate_next(p);
     gate_box.slices = ns;
     CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * (kSlices + 1)));
     CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * (kSlices + 1)));
@@ -1149,12 +1152,18 @@ struct lbgpu_engine {
     gate_state = 1;
     return true;
   }
-  // first box plane of slice c (doubling sizes; the last slice takes the rest)
+  static long long gate_next(long long p) {
+    static constexpr long long kHead[] = {1, 3, 6, 10, 16};  // then +8
+    for (long long h : kHead)
+      if (p < h) return h;
+    return p + 8;
+  }
+  // first box plane of slice c (the last slice takes the rest)
   long long gate_plane(int c) const {
     const long long nzb = gate_box.bz1 - gate_box.bz0;
     if (c >= gate_box.slices) return nzb;
     long long p = 0;
-    for (int k = 0; k < c; ++k) p += std::max<long long>(1, p);
+    for (int k = 0; k < c; ++k) p = gate_next(p);
     return std::min(p, nzb);
   }
   // The gated fused sweep of a deferred pair (adj_pending): one k_pair launch
@@ -1354,7 +1363,10 @@ struct lbgpu_engine {
   // f^{n+1} gathered once, FP64); otherwise the sweeps run apart. Residuals
   // (nullable) are those of the last pair.
   // Fused pairs win at FP64 only (FP32 measured slower than the sweeps apart).
-  bool fuse_pairs() const { return !exact && (prec == 64 || aa); }
+#ifndef LBGPU_FUSE_FP32
+#define LBGPU_FUSE_FP32 0  // FP32 double-buffered pairs run apart (measured faster)
+#endif
+  bool fuse_pairs() const { return !exact && (prec == 64 || aa || LBGPU_FUSE_FP32); }
   void fused_pair_raw(bool resid) {
     ++primal_steps;
     ++adjoint_steps;

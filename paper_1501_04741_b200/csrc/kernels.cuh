@@ -1460,10 +1460,11 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
     const Gate& gt = a.gate;
     if (z >= gt.bz0 && z < gt.bz1) {
       if (threadIdx.x == 0 && threadIdx.y == 0) {
-        // slices of doubling plane counts (engine.cu gate_plane): plane q is
-        // in slice floor(log2 q) + 1 (q = 0: slice 0), the last one open-ended
+        // slice boundaries 0, 1, 3, 6, 10, 16, 24, 32, ... (engine.cu
+        // gate_next), the last slice open-ended
         const int q = z - gt.bz0;
-        const int c = q == 0 ? 0 : min(32 - __clz(q), gt.slices - 1);
+        const int c0 = q < 1 ? 0 : q < 3 ? 1 : q < 6 ? 2 : q < 10 ? 3 : q < 16 ? 4 : 5 + (q - 16) / 8;
+        const int c = min(c0, gt.slices - 1);
         const volatile unsigned* fl = gt.flags + c;
         // bounded (~2 s): a slice that never lands is reported, never a hang
         for (unsigned it = 0; *fl < gt.seq; ++it) {

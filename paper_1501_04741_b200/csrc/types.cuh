@@ -51,8 +51,8 @@ struct Push {
 // design nodes form the box [bx0,bx1) x [by0,by1) x [bz0,bz1) (interior x the
 // design x-range, config.cpp:347-371), whose design values arrive in
 // DesignField::nodes order in wd, in `slices` groups of whole box z-planes
-// (1, 1, 2, 4, 8, ... planes, the last taking the rest), flags[c] reaching
-// `seq` when slice c has landed. A block whose z-plane is
+// (1, 2, 3, 4, 6 planes, then 8 each, the last taking the rest), flags[c]
+// reaching `seq` when slice c has landed. A block whose z-plane is
 // in the box waits for its slice, reads its nodes' new w from wd and also
 // writes them into the full-grid design buffer w_out.
 struct Gate {

@@ -57,7 +57,9 @@ for k, v in c3.items():
     L.append(f"| {k} | {v['primal_mlups']:,.0f} ({v['primal_gbs']:,.0f}) | {v['adjoint_mlups']:,.0f} "
              f"({v['adjoint_gbs']:,.0f}) | {v.get('pair_mlups', float('nan')):,.0f} | "
              f"{v.get('adjoint_frozen_base_mlups', float('nan')):,.0f} |")
-L.append("\nMeasured copy peak: 6,548.8 GB/s. The pair is fused (one k_pair sweep) at FP64 and runs "
+_pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6529.4
+L.append(f"\nMeasured copy peak: {_pk:,.1f} GB/s. The pair is fused (one k_pair sweep) at FP64 and runs "
          "apart at FP32.\n")
 L.append("## C4: 512x128x128 exchanger3d topology optimisation\n")
 for key, title in (("parity_128x32x32", "128x32x32 (C4 proportions)"),
@@ -73,7 +75,8 @@ for key, title in (("parity_128x32x32", "128x32x32 (C4 proportions)"),
                  f"- reference {p['reference_seconds_1thread']:.1f} s on 1 thread.\n")
 L.append(f"**Throughput.**\n- One-shot: {c4['one_shot_iterations_per_s']:.0f} iterations/s, i.e. "
          f"{c4['one_shot_node_iterations_mlups']:,.0f} M node-iterations/s. Each iteration is "
-         "primal + adjoint + fused gradient/update.\n"
+         "primal + adjoint + gradient/update; the update of a non-record iteration rides in the "
+         "next iteration's primal sweep (k_primal UPD).\n"
          f"- Sweeps: primal {c4['primal_gbs']:,.0f} GB/s, adjoint {c4['adjoint_gbs']:,.0f} GB/s.\n"
          f"- The reference on {c4['reference_cores']} threads: "
          f"{c4['reference_primal_plus_adjoint_seconds_per_iteration']:.2f} s per primal+adjoint "
