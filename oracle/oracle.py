@@ -314,6 +314,9 @@ def _load_ref():
         L.ref_time.argtypes = [vp, C.c_int, C.c_int, C.c_long, C.POINTER(C.c_double)]
         L.ref_partitioned.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, _DP]
         L.ref_objective_enabled.argtypes = [vp, C.c_int]
+        L.ref_partitioned_solve.argtypes = [vp, C.c_int, C.c_double, C.c_long, C.c_long,
+                                            C.POINTER(C.c_long), C.POINTER(C.c_double),
+                                            C.POINTER(C.c_int)]
         L.ref_tangent.argtypes = [vp, vp, C.c_double, C.c_double, C.c_long,
                                   C.POINTER(C.c_double), C.POINTER(C.c_long),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -467,6 +470,15 @@ class RefOracle:
         r = np.zeros(2)
         self._ok(self.L.ref_partitioned(self.h, threads, n_primal, n_adjoint, n_pairs, r))
         return float(r[0]), float(r[1])
+
+    def partitioned_solve(self, threads: int, tol: float, max_iter: int = 200000,
+                          fixed: int = -1):
+        """partitioned_fixed_point on `threads` host threads from the handle's
+        f: (iterations, residual, converged); f gathered back."""
+        it, res, conv = C.c_long(), C.c_double(), C.c_int()
+        self._ok(self.L.ref_partitioned_solve(self.h, threads, tol, max_iter, fixed, C.byref(it),
+                                              C.byref(res), C.byref(conv)))
+        return it.value, res.value, bool(conv.value)
 
     def objective_enabled(self, on: bool) -> None:
         """obj_empty of the A14 composition recipe: adjoint steps without

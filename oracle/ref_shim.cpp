@@ -400,6 +400,28 @@ int ref_partitioned(void* h, int threads, long n_primal, long n_adjoint, long n_
   });
 }
 
+// partitioned_fixed_point (partition.cpp:279-312): the reference's
+// tol-stop primal solve on its thread-per-slab runner (bitwise its
+// monolithic solve_fixed_point), from the handle's f; the state is gathered
+// back into the handle.
+int ref_partitioned_solve(void* h, int threads, double tol, long max_iter, long fixed,
+                          long* iters, double* res, int* conv) {
+  return guard([&] {
+    std::visit([&](auto& F) {
+      using R = std::decay_t<decltype(F.f.raw(0)[0])>;
+      SolveOptions<R> o;
+      o.tol = tol;
+      o.max_iter = max_iter;
+      o.fixed_iters = fixed;
+      const SolveResult r =
+          partitioned_fixed_point<R>(H(h)->bc.sys, H(h)->bc.objective, F.f, threads, o);
+      *iters = r.iterations;
+      *res = r.residual;
+      *conv = r.converged ? 1 : 0;
+    }, H(h)->fl);
+  });
+}
+
 // The A14 composition recipe's obj_empty: on = 0 clears the
 // objective's full-grid membership flags so adjoint_step skips the source
 // term (adjoint.cpp:199); on = 1 restores them from the support list.

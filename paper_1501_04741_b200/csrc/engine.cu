@@ -1116,7 +1116,7 @@ struct lbgpu_engine {
   // fused sweep of a deferred pair is ONE launch whose blocks wait on
   // per-slice flags the copy engine sets behind each slice of the upload --
   // no z-chunk kernel boundaries, no scatter kernels.
-  static constexpr int kSlices = 24;
+  static constexpr int kSlices = 6;
   int gate_state = -1;  // -1 unknown, 0 no box, 1 box
   Gate gate_box{};
   unsigned* d_gate_flags = nullptr;  // [kSlices] flags, then the timeout word
@@ -1136,15 +1136,24 @@ struct lbgpu_engine {
     if (vol != (long long)design.size()) return false;  // not a box: the chunked path
     gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
     gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
-    // slices of 1, 2, 3, 4, 6 box planes, then 8 each: the first lands within
-    // microseconds, and every later one before the sweep reaches its first
-    // plane (the upload moves ~1.6 planes per plane the sweep finishes, so a
-    // slice [a, b) is never waited for once b / a < 1.6; measured: equal
-    // 8-plane slices wait ~25 us for the first, doubling sizes wait on the
-    // large last ones)
+    // six slices growing ~1.7x (3%, 8%, 13%, 19%, 30%, 27% of the planes):
+    // the host enqueues them before the launch, so the copy engine starts
+    // ahead of the sweep, lands each slice before the sweep reaches it (the
+    // upload moves ~1.6 planes per plane swept), and the enqueue itself is 12
+    // calls. (Measured: 16 equal slices cost ~90 us of enqueue before the
+    // launch; doubling sizes made the sweep wait on the large last ones.)
+    static constexpr double kFrac[kSlices + 1] = {0.0, 0.032, 0.111, 0.238, 0.429, 0.730, 1.0};
     const int nzb = z1_ - z0_ + 1;
     int ns = 0;
-    for (long long p = 0; p < nzb && ns < kSlices - 1; ++ns) p = gate_next(p);
+    gate_box.bnd[0] = 0;
+    for (int c = 1; c <= kSlices; ++c) {
+      const int b = std::max(gate_box.bnd[ns] + 1, int(std::lround(kFrac[c] * nzb)));
+      if (b >= nzb || c == kSlices) {
+        gate_box.bnd[++ns] = nzb;
+        break;
+      }
+      gate_box.bnd[++ns] = b;
+    }
     gate_box.slices = ns;
     CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * (kSlices + 1)));
     CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * (kSlices + 1)));
@@ -1152,31 +1161,19 @@ struct lbgpu_engine {
     gate_state = 1;
     return true;
   }
-  static long long gate_next(long long p) {
-    static constexpr long long kHead[] = {1, 3, 6, 10, 16};  // then +8
-    for (long long h : kHead)
-      if (p < h) return h;
-    return p + 8;
-  }
-  // first box plane of slice c (the last slice takes the rest)
-  long long gate_plane(int c) const {
-    const long long nzb = gate_box.bz1 - gate_box.bz0;
-    if (c >= gate_box.slices) return nzb;
-    long long p = 0;
-    for (int k = 0; k < c; ++k) p = gate_next(p);
-    return std::min(p, nzb);
-  }
-  // The gated fused sweep of a deferred pair (adj_pending): one k_pair launch
-  // on st, issued FIRST so the GPU starts as soon as slice 0 lands, then the
-  // upload slices + flags on the copy stream (which waits only for the work
-  // queued before this call: the previous call's readers of d_wvals).
+  long long gate_plane(int c) const { return gate_box.bnd[std::min(c, gate_box.slices)]; }
+  // The gated fused sweep of a deferred pair (adj_pending): the upload slices
+  // + flags on the copy stream (which waits only for the work queued before
+  // this call: the previous call's readers of d_wvals), THEN one k_pair launch
+  // on st. Enqueueing the copies first keeps the scheme deadlock-free where
+  // launches serialise with copies (CUDA_LAUNCH_BLOCKING, profilers): every
+  // slice is then already in flight when the sweep starts.
   void gated_pair(const double* wd) {
     ensure_h2d();
     CU(cudaEventRecord(ev_chunk[kChunks], st));
     ++gate_seq;
     const int ns = gate_box.slices;
     CU(cudaMemsetAsync(d_gate_flags + kSlices, 0, sizeof(unsigned), st));
-    gated_launch();
     CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
     const long long plane = (long long)(gate_box.bx1 - gate_box.bx0) * (gate_box.by1 - gate_box.by0);
     for (int c = 0; c < ns; ++c) {
@@ -1188,6 +1185,7 @@ struct lbgpu_engine {
       CU(cudaMemcpyAsync(d_gate_flags + c, h_gate_seq + c, sizeof(unsigned), cudaMemcpyHostToDevice,
                          st_h2d));
     }
+    gated_launch();
   }
   void gated_launch() {
     NodeTables tn = T;

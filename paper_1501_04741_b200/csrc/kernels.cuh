@@ -1460,19 +1460,21 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
     const Gate& gt = a.gate;
     if (z >= gt.bz0 && z < gt.bz1) {
       if (threadIdx.x == 0 && threadIdx.y == 0) {
-        // slice boundaries 0, 1, 3, 6, 10, 16, 24, 32, ... (engine.cu
-        // gate_next), the last slice open-ended
         const int q = z - gt.bz0;
-        const int c0 = q < 1 ? 0 : q < 3 ? 1 : q < 6 ? 2 : q < 10 ? 3 : q < 16 ? 4 : 5 + (q - 16) / 8;
-        const int c = min(c0, gt.slices - 1);
+        int c = 0;
+        while (c + 1 < gt.slices && gt.bnd[c + 1] <= q) ++c;
         const volatile unsigned* fl = gt.flags + c;
-        // bounded (~2 s): a slice that never lands is reported, never a hang
-        for (unsigned it = 0; *fl < gt.seq; ++it) {
-          if (it > (1u << 23)) {
+        // bounded (0.5 s of wall time): a slice that never lands is reported
+        // (LBGPU_E_NUMERIC at the call), never a hang
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (*fl < gt.seq) {
+          __nanosleep(256);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 500000000ull) {
             atomicExch(gt.err, 1u);
             break;
           }
-          __nanosleep(256);
         }
         __threadfence();
       }

@@ -51,7 +51,7 @@ struct Push {
 // design nodes form the box [bx0,bx1) x [by0,by1) x [bz0,bz1) (interior x the
 // design x-range, config.cpp:347-371), whose design values arrive in
 // DesignField::nodes order in wd, in `slices` groups of whole box z-planes
-// (1, 2, 3, 4, 6 planes, then 8 each, the last taking the rest), flags[c]
+// (slice c = box planes [bnd[c], bnd[c+1]), sizes growing ~1.7x), flags[c]
 // reaching `seq` when slice c has landed. A block whose z-plane is
 // in the box waits for its slice, reads its nodes' new w from wd and also
 // writes them into the full-grid design buffer w_out.
@@ -62,6 +62,7 @@ struct Gate {
   unsigned* err = nullptr;  // set when a slice never landed (bounded wait)
   unsigned seq = 0;
   int slices = 0;
+  int bnd[9] = {};
   int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;
 };
 

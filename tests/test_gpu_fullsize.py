@@ -159,6 +159,30 @@ def test_c1_fixed_iteration_parity(lbgpu, oracle_mod, has_gpu):
         e.close()
 
 
+def test_c1_tol_stop_iteration_parity(lbgpu, oracle_mod, has_gpu):
+    """the tol-stop iteration of solve_fixed_point
+    (collision.cpp:377-416) at C1 size against the reference's own stop rule,
+    run on its partitioned_fixed_point (partition.cpp:279-312, bitwise its
+    monolithic solve) on the host threads. tol 1e-6 (crossed near 10^5 steps)
+    rather than SURVEY's 1e-7 (near 3*10^5, ~30 min of reference CPU time);
+    bit-exact build: the same iteration, residual and state; product build:
+    the iteration within +-1."""
+    txt = cfg("C1")
+    r = oracle_mod.RefOracle(txt)
+    r.init_state()
+    it_r, res_r, conv_r = r.partitioned_solve(min(THREADS, 16), 1e-6, 3000000)
+    assert conv_r and it_r > 10000
+    x = lbgpu.Engine.from_config(txt, exact=True)
+    x.init_state()
+    it_x, res_x, conv_x = x.solve_primal(1e-6, 3000000)
+    assert (it_x, res_x, conv_x) == (it_r, res_r, conv_r)
+    assert np.array_equal(x.get_state(0), r.get_state(0))
+    e = lbgpu.Engine.from_config(txt)
+    e.init_state()
+    it_e, res_e, conv_e = e.solve_primal(1e-6, 3000000)
+    assert conv_e and abs(it_e - it_r) <= 1
+
+
 def _warm_one_shot(lbgpu, oracle_mod, txt_warm, txt_run, warm, iters):
     g = lbgpu.Engine.from_config(txt_warm)
     g.init_state()

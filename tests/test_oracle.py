@@ -164,3 +164,16 @@ def test_partitioned_runner_equals_monolithic(oracle_mod, name):
     a.objective_enabled(True)
     a.adjoint_steps(1)
     assert np.any(a.get_state(1))
+
+
+def test_partitioned_solve_equals_monolithic(oracle_mod):
+    """ref_partitioned_solve is the reference's partitioned_fixed_point:
+    the same stop iteration, residual and state as solve_fixed_point."""
+    O = oracle_mod
+    _need_ref(O)
+    txt = case_text("grad2d")
+    a, b = O.RefOracle(txt), O.RefOracle(txt)
+    a.init_state()
+    b.init_state()
+    assert a.partitioned_solve(3, 1e-8, 200000) == b.solve_primal(1e-8, 200000)
+    assert np.array_equal(a.get_state(0), b.get_state(0))
