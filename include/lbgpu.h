@@ -213,9 +213,12 @@ int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64
  * lbgpu_adjoint_step(1, kernel 0) + lbgpu_objective bit for bit in everything
  * observable. Residuals and objective are nullable. Without residuals (3D,
  * FP64 product build) the call's adjoint sweep is deferred into the next
- * call's primal sweep (one fused kernel reading f once, gated on the upload
- * slices); every other lbgpu call, or lbgpu_finish, completes it first. A
- * rho <= 0 inside a deferred sweep is reported by the call that runs it. */
+ * call's primal sweep (one fused kernel reading f once, each design node's
+ * thread waiting for its own uploaded value); every other lbgpu call, or
+ * lbgpu_finish, completes it first. A rho <= 0 inside a deferred sweep is
+ * reported by the call that runs it. The gated sweep takes a value equal to
+ * the bit pattern 0x7ff4dead0000beef (a NaN) as "not landed yet": such a
+ * value fails the call (LBGPU_E_NUMERIC) after a bounded wait. */
 int lbgpu_pair_step_with_design(lbgpu_engine* e, const double* w_design, double* primal_residual,
                                 double* adjoint_residual, double* objective);
 /* Complete any deferred sweep and wait for the engine's stream. */

@@ -163,8 +163,14 @@ void model_rows(std::vector<double>& U, std::vector<int>& cls) {
 // by height (all children one level down or more) and each level runs in
 // parallel — wide levels as their own launch, the narrow top of the tree in
 // one block with a barrier per level.
+__global__ void __launch_bounds__(1024) k_tree_small(const double* __restrict__, const long long* __restrict__,
+                             const long long* __restrict__, int, const int2* __restrict__,
+                             const int* __restrict__, int, int, double*);
 struct PairTree {
   static constexpr int kTopOps = 2048;  // levels narrower than this: single-block kernel
+  static constexpr size_t kSmallMax = 160 * 1024;  // whole tree in one block's shared memory
+  size_t small_bytes = 0;
+  bool small() const { return small_bytes <= kSmallMax; }
   long long n = -1;
   int leaves = 0, ops = 0;
   long long* d_lo = nullptr;
@@ -209,6 +215,15 @@ struct PairTree {
     for (int k = 0; k < ops; ++k) o[pos[k]] = make_int2(dec(tmp[k].first), dec(tmp[k].second));
     top = levels;
     while (top > 0 && lvl[top] - lvl[top - 1] < kTopOps) --top;  // levels top+1.. are narrow
+    small_bytes = size_t(leaves + ops) * sizeof(double) + size_t(ops) * sizeof(int2) +
+                  size_t(levels + 1) * sizeof(int);
+    if (small_bytes <= kSmallMax) {
+      static bool attr = false;
+      if (!attr) {
+        CU(cudaFuncSetAttribute(k_tree_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmallMax)));
+        attr = true;
+      }
+    }
     CU(cudaMalloc(&d_lo, sizeof(long long) * leaves));
     CU(cudaMalloc(&d_hi, sizeof(long long) * leaves));
     CU(cudaMalloc(&d_vals, sizeof(double) * (leaves + ops + 1)));
@@ -254,6 +269,57 @@ __global__ void __launch_bounds__(1024) k_combine_top(double* vals, const int2* 
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = nops ? vals[leaves + nops - 1] : vals[0];
+}
+
+// A whole small tree in one block (the objective's support plane: ~1K leaves):
+// the leaf sums (each leaf's <= 16 terms loaded at once, then added in the
+// reference's left-to-right order), every level's combines in shared memory,
+// the root to *out. Same additions on the same operands as k_leaf_sums +
+// k_combine_top, so the same bits; one launch and no global round trip per level.
+constexpr int kLeafMax = 16;
+__global__ void __launch_bounds__(1024) k_tree_small(const double* __restrict__ t,
+                                                     const long long* __restrict__ lo,
+                                                     const long long* __restrict__ hi, int leaves,
+                                                     const int2* __restrict__ ops,
+                                                     const int* __restrict__ lvl, int levels,
+                                                     int nops, double* out) {
+  extern __shared__ double sv[];  // [leaves + ops] values, then the ops, then lvl
+  int2* sop = reinterpret_cast<int2*>(sv + leaves + nops);
+  int* slv = reinterpret_cast<int*>(sop + nops);
+  for (int k = threadIdx.x; k < nops; k += blockDim.x) sop[k] = ops[k];
+  for (int k = threadIdx.x; k <= levels && nops; k += blockDim.x) slv[k] = lvl[k];
+  for (int i = threadIdx.x; i < leaves; i += blockDim.x) {
+    const long long b = lo[i];
+    const int m = int(hi[i] - b);
+    double x[kLeafMax];
+#pragma unroll
+    for (int k = 0; k < kLeafMax; ++k) x[k] = k < m ? t[b + k] : 0.0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kLeafMax; ++k)
+      if (k < m) s += x[k];
+    sv[i] = s;
+  }
+  __syncthreads();
+  for (int h = 1; h <= levels; ++h) {
+    for (int k = slv[h - 1] + threadIdx.x; k < slv[h]; k += blockDim.x) {
+      const int2 o = sop[k];
+      sv[leaves + k] = sv[o.x] + sv[o.y];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = nops ? sv[leaves + nops - 1] : sv[0];
+}
+
+// The flag words' start values (a kernel: no pageable-memory copy per call).
+__global__ void k_reset_flags(unsigned long long* fl) {
+  const int i = threadIdx.x;
+  if (i < 6) fl[i] = (i == 1 || i == 3) ? kNoBad : 0ull;
+}
+
+__global__ void k_fill_bits(unsigned long long* p, long long n, unsigned long long v) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
 }
 
 __global__ void k_scatter_design(const double* __restrict__ vals, const long long* __restrict__ nodes,
@@ -347,7 +413,8 @@ struct lbgpu_engine {
   double* d_ref = nullptr;
   double* d_wvals = nullptr;  // staging for design-order uploads
   bool w_host_stale = false;  // device w moved ahead of the host copy
-  unsigned long long* d_flags = nullptr;  // [resid, bad, aux]
+  // [resid, bad, aux, adjoint bad, J (bits), upload timeout]: one D2H read per call
+  unsigned long long* d_flags = nullptr;
   unsigned long long* d_ring = nullptr;   // per-step residual ring for batched solves
   unsigned long long* h_flags = nullptr;  // pinned mirror
   PairTree tree_support, tree_design, tree_inlet;
@@ -385,8 +452,7 @@ struct lbgpu_engine {
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
     cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals), cudaFree(d_w2);
-    cudaFree(d_gate_flags);
-    if (h_gate_seq) cudaFreeHost(h_gate_seq);
+    cudaFree(d_wgate);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -519,7 +585,7 @@ struct lbgpu_engine {
     CU(cudaMalloc(&d_terms, sizeof(double) * nt));
     CU(cudaMalloc(&d_grad, sizeof(double) * std::max<size_t>(design.size(), 1)));
     CU(cudaMalloc(&d_scalar, sizeof(double) * 4));
-    CU(cudaMalloc(&d_flags, sizeof(unsigned long long) * 4));
+    CU(cudaMalloc(&d_flags, sizeof(unsigned long long) * 6));
     CU(cudaMalloc(&d_ring, sizeof(unsigned long long) * kRing));
     CU(cudaMallocHost(&h_flags, sizeof(unsigned long long) * (4 + kRing)));
     tree_support.build((long long)support.size());
@@ -665,8 +731,7 @@ struct lbgpu_engine {
   // d_flags: [0] residual, [1] first bad node (primal, or the call's only
   // sweep kind), [2] aux, [3] first bad node of the adjoint half of a pair call
   void reset_flags() {
-    const unsigned long long init[4] = {0ull, kNoBad, 0ull, kNoBad};
-    CU(cudaMemcpyAsync(d_flags, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_reset_flags<<<1, 32, 0, st>>>(d_flags);
     kb_p = primal_steps, kb_a = adjoint_steps, kb_t = tangent_steps;
   }
   // step: the sweep's number relative to the current key base (1-based)
@@ -1113,15 +1178,14 @@ struct lbgpu_engine {
   bool w2_synced = false;
   // Upload-gated single launch (kernels.cuh Gate): when the design nodes are
   // exactly a box (config-built cases: interior x the design x-range), the
-  // fused sweep of a deferred pair is ONE launch whose blocks wait on
-  // per-slice flags the copy engine sets behind each slice of the upload --
-  // no z-chunk kernel boundaries, no scatter kernels.
-  static constexpr int kSlices = 6;
+  // fused sweep of a deferred pair is ONE launch behind ONE H2D copy of the
+  // design vector into d_wgate: each box node's thread waits for its own value
+  // to replace the sentinel and re-arms the entry -- no slices, no flags, no
+  // z-chunk kernel boundaries, no scatter kernels.
   int gate_state = -1;  // -1 unknown, 0 no box, 1 box
   Gate gate_box{};
-  unsigned* d_gate_flags = nullptr;  // [kSlices] flags, then the timeout word
-  unsigned* h_gate_seq = nullptr;  // pinned source of the flag values
-  unsigned gate_seq = 0;
+  double* d_wgate = nullptr;  // design-order upload buffer, kGateEmpty between uploads
+  bool gate_armed = false;
   bool gate_ready() {
     if (gate_state >= 0) return gate_state == 1;
     gate_state = 0;
@@ -1136,67 +1200,37 @@ struct lbgpu_engine {
     if (vol != (long long)design.size()) return false;  // not a box: the chunked path
     gate_box.bx0 = x0_, gate_box.bx1 = x1_ + 1, gate_box.by0 = y0_, gate_box.by1 = y1_ + 1;
     gate_box.bz0 = z0_, gate_box.bz1 = z1_ + 1;
-    // six slices growing ~1.7x (3%, 8%, 13%, 19%, 30%, 27% of the planes):
-    // the host enqueues them before the launch, so the copy engine starts
-    // ahead of the sweep, lands each slice before the sweep reaches it (the
-    // upload moves ~1.6 planes per plane swept), and the enqueue itself is 12
-    // calls. (Measured: 16 equal slices cost ~90 us of enqueue before the
-    // launch; doubling sizes made the sweep wait on the large last ones.)
-    static constexpr double kFrac[kSlices + 1] = {0.0, 0.032, 0.111, 0.238, 0.429, 0.730, 1.0};
-    const int nzb = z1_ - z0_ + 1;
-    int ns = 0;
-    gate_box.bnd[0] = 0;
-    for (int c = 1; c <= kSlices; ++c) {
-      const int b = std::max(gate_box.bnd[ns] + 1, int(std::lround(kFrac[c] * nzb)));
-      if (b >= nzb || c == kSlices) {
-        gate_box.bnd[++ns] = nzb;
-        break;
-      }
-      gate_box.bnd[++ns] = b;
-    }
-    gate_box.slices = ns;
-    CU(cudaMalloc(&d_gate_flags, sizeof(unsigned) * (kSlices + 1)));
-    CU(cudaMemset(d_gate_flags, 0, sizeof(unsigned) * (kSlices + 1)));
-    CU(cudaMallocHost(&h_gate_seq, sizeof(unsigned) * (kSlices + 1)));
+    CU(cudaMalloc(&d_wgate, sizeof(double) * design.size()));
+    gate_armed = false;
     gate_state = 1;
     return true;
   }
-  long long gate_plane(int c) const { return gate_box.bnd[std::min(c, gate_box.slices)]; }
-  // The gated fused sweep of a deferred pair (adj_pending): the upload slices
-  // + flags on the copy stream (which waits only for the work queued before
-  // this call: the previous call's readers of d_wvals), THEN one k_pair launch
-  // on st. Enqueueing the copies first keeps the scheme deadlock-free where
-  // launches serialise with copies (CUDA_LAUNCH_BLOCKING, profilers): every
-  // slice is then already in flight when the sweep starts.
+  // The gated fused sweep of a deferred pair (adj_pending): the upload on the
+  // copy stream (which waits for the work queued before this call: the
+  // previous sweep's re-arming of d_wgate), THEN one k_pair launch on st.
+  // Enqueueing the copy first keeps the scheme deadlock-free where launches
+  // serialise with copies (CUDA_LAUNCH_BLOCKING, profilers): the values are
+  // then in place when the sweep starts.
   void gated_pair(const double* wd) {
     ensure_h2d();
-    CU(cudaEventRecord(ev_chunk[kChunks], st));
-    ++gate_seq;
-    const int ns = gate_box.slices;
-    CU(cudaMemsetAsync(d_gate_flags + kSlices, 0, sizeof(unsigned), st));
-    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
-    const long long plane = (long long)(gate_box.bx1 - gate_box.bx0) * (gate_box.by1 - gate_box.by0);
-    for (int c = 0; c < ns; ++c) {
-      const long long p0 = gate_plane(c), p1 = gate_plane(c + 1);
-      if (p1 > p0)
-        CU(cudaMemcpyAsync(d_wvals + p0 * plane, wd + p0 * plane, sizeof(double) * (p1 - p0) * plane,
-                           cudaMemcpyHostToDevice, st_h2d));
-      h_gate_seq[c] = gate_seq;
-      CU(cudaMemcpyAsync(d_gate_flags + c, h_gate_seq + c, sizeof(unsigned), cudaMemcpyHostToDevice,
-                         st_h2d));
+    const long long n = (long long)design.size();
+    if (!gate_armed) {  // first use, or after a timed-out upload
+      k_fill_bits<<<unsigned((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_wgate),
+                                                             n, kGateEmpty);
+      ++launches;
     }
-    gated_launch();
-  }
-  void gated_launch() {
+    CU(cudaEventRecord(ev_chunk[kChunks], st));
+    CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
+    CU(cudaMemcpyAsync(d_wgate, wd, sizeof(double) * n, cudaMemcpyHostToDevice, st_h2d));
+    gate_armed = false;  // until the sweep is known to have re-armed every entry
     NodeTables tn = T;
     tn.w = d_w2;     // the new design's full-grid buffer (design nodes written by the sweep)
     tn.w_adj = d_w;  // the previous design (the deferred adjoint half)
     SweepArgs sa = sweep(primal_steps - kb_p, false, nullptr);
     sa.a.t = tn;
     sa.a.gate = gate_box;
-    sa.a.gate.wd = d_wvals, sa.a.gate.w_out = d_w2, sa.a.gate.flags = d_gate_flags;
-    sa.a.gate.err = d_gate_flags + kSlices;
-    sa.a.gate.seq = gate_seq;
+    sa.a.gate.wd = d_wgate, sa.a.gate.w_out = d_w2;
+    sa.a.gate.err = reinterpret_cast<unsigned*>(d_flags + 5);  // cleared by reset_flags
     sa.dualw = true;
     fast::pair(sa, f[fc], f[1 - fc], v[vc], v[1 - vc]);
     launches += 1 + (sa.n_adj_side > 0);
@@ -1231,7 +1265,6 @@ struct lbgpu_engine {
     if (fuse) ++adjoint_steps;
     const bool gated = fuse && gate_ready();
     if (gated) {
-      ensure_h2d();
       gated_pair(wd);
     } else {
       queue_design_upload(wd, ib, zb, true, true);
@@ -1270,23 +1303,20 @@ struct lbgpu_engine {
       fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support,
                             (long long)support.size(), d_terms, 0);
       ++launches;
-      pairwise_queue(tree_support, d_terms);
+      pairwise_queue(tree_support, d_terms, reinterpret_cast<double*>(d_flags + 4));
       if (trace_on()) trace("J", st);
     }
     CU(cudaGetLastError());
     reduce_flags(d_flags + 1, 1, true);
-    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
-    if (J) CU(cudaMemcpyAsync(h_flags + 5, d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (gated)
-      CU(cudaMemcpyAsync(h_gate_seq + kSlices, d_gate_flags + kSlices, sizeof(unsigned),
-                         cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
     sync();  // one host sync per call; the host design buffer is consumed too
     trace_print();
-    if (gated && h_gate_seq[kSlices])
+    if (gated && !h_flags[5]) gate_armed = true;
+    if (gated && h_flags[5])
       throw Fail{LBGPU_E_NUMERIC, "design upload: a slice did not land within the sweep's wait bound"};
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], fuse ? "iteration (or the deferred adjoint iteration)" : "iteration");
     adj_pending = true;
-    if (J) *J = bits_to_double(h_flags[5]);
+    if (J) *J = bits_to_double(h_flags[4]);
   }
 
   // New design values (DesignField::nodes order, host memory) followed by n
@@ -1767,8 +1797,7 @@ struct lbgpu_engine {
           const Launch a = launch(primal_steps - kb_p);
           if (exact) exact::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms, 0);
           else fast::objective_terms(a, dim, prec, f[fc], d_support, (long long)support.size(), d_terms, 0);
-          pairwise_queue(tree_support, d_terms);
-          CU(cudaMemcpyAsync(d_vals + 2 * k + side, d_scalar, sizeof(double), cudaMemcpyDeviceToDevice, st));
+          pairwise_queue(tree_support, d_terms, d_vals + 2 * k + side);
         }
         if (idx < 0) {
           set_rho_in(rho0);
@@ -1804,8 +1833,15 @@ struct lbgpu_engine {
     sync();
     return out;
   }
-  // the tree replay only; the sum lands in d_scalar[0]
-  void pairwise_queue(PairTree& tr, const double* d_t) {
+  // the tree replay only; the sum lands in *out (default d_scalar[0])
+  void pairwise_queue(PairTree& tr, const double* d_t, double* out = nullptr) {
+    if (!out) out = d_scalar;
+    if (tr.small()) {
+      k_tree_small<<<1, 1024, tr.small_bytes, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_ops, tr.d_lvl,
+                                                     int(tr.lvl.size()) - 1, tr.ops, out);
+      ++launches;
+      return;
+    }
     const int nb = (tr.leaves + 127) / 128;
     k_leaf_sums<<<nb, 128, 0, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_vals);
     for (int h = 1; h <= tr.top; ++h) {
@@ -1813,7 +1849,7 @@ struct lbgpu_engine {
       k_combine_level<<<unsigned((e - b + 255) / 256), 256, 0, st>>>(tr.d_vals, tr.d_ops, tr.leaves, b, e);
     }
     k_combine_top<<<1, 1024, 0, st>>>(tr.d_vals, tr.d_ops, tr.d_lvl, tr.leaves, tr.top,
-                                      int(tr.lvl.size()) - 1, tr.ops, d_scalar);
+                                      int(tr.lvl.size()) - 1, tr.ops, out);
     launches += 2 + tr.top;
   }
   double objective(const void* buf = nullptr) {

@@ -986,8 +986,16 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 // owned columns of the 3-D grid, or, with c0 >= 0, over the slab's two
 // boundary columns c0, c1 only (one thread per (column, y, z); a runtime
 // switch, uniform per launch, to halve the instantiations).
+// Register bound of the in-place primal (FP64): left alone, the sweep from E
+// keeps its 26 scattered store addresses live across the collision (182
+// registers, 2 blocks/SM). Measured C3 primal GB/s at 1/2/3/4 blocks per SM:
+// 5,543 / 5,535 / 5,922 / 5,648 (4: 248 B of spill).
+#ifndef LBGPU_AA_PRIMAL_MINB
+#define LBGPU_AA_PRIMAL_MINB 3
+#endif
 template <class L, class R, int CK, int FM>
-__global__ void __launch_bounds__(128) k_primal_aa(Launch a, R* A, int c0, int c1) {
+__global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : 1)
+    k_primal_aa(Launch a, R* A, int c0, int c1) {
   unsigned long long rmax = 0;
   if (c0 >= 0) {
     const long long yz = (long long)a.g.ny * a.g.nz;
@@ -1220,8 +1228,15 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
 
 // In-place adjoint sweep (AA streaming, fast build): base f read under BM, v
 // updated in place from layout VM; COLS as k_primal_aa.
+// In-place adjoint (FP64), C3 GB/s at 2/3/4 blocks per SM: 4,947 / 5,988 /
+// 5,824 (4 spills 144-472 B in the sweeps from E).
+#ifndef LBGPU_AA_ADJ_MINB
+#define LBGPU_AA_ADJ_MINB 3
+#endif
 template <class L, class R, int CK, int BM, int VM, bool MOM>
-__global__ void LBGPU_ADJ_BOUNDS(true, R, MOM) k_adjoint_aa(Launch a, const R* __restrict__ base,
+__global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_ADJ_MINB
+                                                      : (MOM ? LBGPU_ADJ_MINB32_MOM : LBGPU_ADJ_MINB32))
+    k_adjoint_aa(Launch a, const R* __restrict__ base,
                                                             R* V, const R* __restrict__ mom,
                                                             int c0, int c1) {
   unsigned long long rmax = 0;
@@ -1290,6 +1305,36 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
 template <class R>
 constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 
+// Take a design-box node's uploaded value: poll its entry of the upload
+// buffer until the copy engine has replaced the sentinel, then re-arm it.
+// Relaxed loads (L2, no fence, no block barrier: the node's gather stays in
+// flight); the sweep runs in z order behind the upload, so the first load
+// almost always passes. Bounded (0.5 s of wall time): a value that never lands
+// is reported (LBGPU_E_NUMERIC at the call), never a hang.
+__device__ __forceinline__ double gate_take(const Gate& gt, long long o) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(gt.wd + o);
+  auto load = [p] {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+  };
+  unsigned long long v = load();
+  if (v == kGateEmpty) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((v = load()) == kGateEmpty) {
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 500000000ull) {
+        atomicExch(gt.err, 1u);
+        break;
+      }
+    }
+  }
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kGateEmpty) : "memory");
+  return __longlong_as_double((long long)v);
+}
+
 // Fused primal + adjoint pair (product build): adjoint sweep n (base
 // f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
 // gathers it once, takes its moments once (node_sums) and the node's
@@ -1302,7 +1347,7 @@ constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 // DUALW: the adjoint half is the previous design's (lbgpu_pair_step_with_design
 // defers each call's adjoint sweep into the next call's fused kernel), so its
 // node constants come from a.t.w_adj while the primal half uses a.t.w -- or,
-// GATED, the just-uploaded design value (a.gate; k_pair waits for its slice).
+// GATED, the just-uploaded design value (a.gate; gate_take waits for it).
 template <class L, class R, int CK, bool RESID, int FM = FM_DB, int VM = FM_DB, bool DUALW = false,
           bool GATED = false>
 __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fdst,
@@ -1333,18 +1378,16 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
   // the node's constants, shared by both halves
   double w = 1.0, omt = 0.0;
   PowPair pp{};
-  if (!bb) {
+  // GATED: a design-box node's w is the just-uploaded value, taken once the
+  // node's gather is in flight
+  bool gated = false;
+  if constexpr (GATED) {
+    const Gate& gt = a.gate;
+    gated = !bb && x >= gt.bx0 && x < gt.bx1 && y >= gt.by0 && y < gt.by1 && z >= gt.bz0 &&
+            z < gt.bz1;
+  }
+  if (!bb && !gated) {
     w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
-    if constexpr (GATED) {
-      const Gate& gt = a.gate;
-      if (x >= gt.bx0 && x < gt.bx1 && y >= gt.by0 && y < gt.by1 && z >= gt.bz0 && z < gt.bz1) {
-        const long long o = (long long)(x - gt.bx0) +
-                            (long long)(gt.bx1 - gt.bx0) *
-                                ((y - gt.by0) + (long long)(gt.by1 - gt.by0) * (z - gt.bz0));
-        w = __ldcg(gt.wd + o);  // landed after this block's flag (L2-coherent load)
-        gt.w_out[idx] = w;
-      }
-    }
     pp = node_pp<false>(a.M, a.t, idx, code, w);
     omt = node_omt<R>(a.M, a.t, code, w);
   }
@@ -1355,6 +1398,18 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
     R f[L::M], out[L::M];
     if constexpr (FM == FM_DB) gather<L, R, -1>(fsrc, N, nb, f);
     else gather_m<L, R, -1, FM>(fsrc, N, idx, nb, f);
+    if constexpr (GATED) {
+      if (gated) {
+        const Gate& gt = a.gate;
+        const long long o = (long long)(x - gt.bx0) +
+                            (long long)(gt.bx1 - gt.bx0) *
+                                ((y - gt.by0) + (long long)(gt.by1 - gt.by0) * (z - gt.bz0));
+        w = gate_take(gt, o);
+        gt.w_out[idx] = w;
+        pp = node_pp<false>(a.M, a.t, idx, code, w);
+        omt = node_omt<R>(a.M, a.t, code, w);
+      }
+    }
     if (tag == TAG_WALL) {
       LBGPU_FOR(P, 0, L::M, { out[P] = f[copp<L>(P)]; });
     } else if (tag == TAG_HEATER) {
@@ -1453,34 +1508,6 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   const int z = a.g.z0 + blockIdx.z;
-  if constexpr (GATED) {
-    // the design values of this block's z-plane: wait for the copy engine to
-    // land their slice (blocks start in z order and the upload outruns the
-    // sweep, so only the first planes' blocks ever wait)
-    const Gate& gt = a.gate;
-    if (z >= gt.bz0 && z < gt.bz1) {
-      if (threadIdx.x == 0 && threadIdx.y == 0) {
-        const int q = z - gt.bz0;
-        int c = 0;
-        while (c + 1 < gt.slices && gt.bnd[c + 1] <= q) ++c;
-        const volatile unsigned* fl = gt.flags + c;
-        // bounded (0.5 s of wall time): a slice that never lands is reported
-        // (LBGPU_E_NUMERIC at the call), never a hang
-        unsigned long long t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        while (*fl < gt.seq) {
-          __nanosleep(256);
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-          if (t - t0 > 500000000ull) {
-            atomicExch(gt.err, 1u);
-            break;
-          }
-        }
-        __threadfence();
-      }
-      __syncthreads();
-    }
-  }
   unsigned long long rP = 0, rA = 0;
   if (x < a.g.x1 && y < a.g.ny)
     pair_body<L, R, CK, RESID, FM_DB, FM_DB, DUALW, GATED>(
@@ -2021,7 +2048,7 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
       dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, nzs);
       bool done = false;
       if constexpr (!RES && L::DIM == 3) {
-        if (s.dualw && a.gate.flags) {
+        if (s.dualw && a.gate.wd) {
           k_pair<L, R, CK, false, true, true><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
           done = true;
         } else if (s.dualw) {

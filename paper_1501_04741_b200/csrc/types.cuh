@@ -49,20 +49,17 @@ struct Push {
 
 // Upload-gated design sweep (the deferred design pair's single launch): the
 // design nodes form the box [bx0,bx1) x [by0,by1) x [bz0,bz1) (interior x the
-// design x-range, config.cpp:347-371), whose design values arrive in
-// DesignField::nodes order in wd, in `slices` groups of whole box z-planes
-// (slice c = box planes [bnd[c], bnd[c+1]), sizes growing ~1.7x), flags[c]
-// reaching `seq` when slice c has landed. A block whose z-plane is
-// in the box waits for its slice, reads its nodes' new w from wd and also
-// writes them into the full-grid design buffer w_out.
+// design x-range, config.cpp:347-371), whose design values arrive by one H2D
+// copy into wd, in DesignField::nodes order. Every entry of wd holds the
+// sentinel kGateEmpty until its value lands: the value is its own flag. A
+// thread whose node is in the box waits for it, takes it (re-arming the entry
+// with the sentinel for the next upload) and writes it into the full-grid
+// design buffer w_out.
+constexpr unsigned long long kGateEmpty = 0x7ff4dead0000beefull;  // a NaN no upload carries
 struct Gate {
-  const double* wd = nullptr;
+  double* wd = nullptr;
   double* w_out = nullptr;
-  const unsigned* flags = nullptr;
-  unsigned* err = nullptr;  // set when a slice never landed (bounded wait)
-  unsigned seq = 0;
-  int slices = 0;
-  int bnd[9] = {};
+  unsigned* err = nullptr;  // set when a value never landed (bounded wait)
   int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;
 };
 

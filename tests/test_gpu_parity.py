@@ -395,6 +395,20 @@ def test_deferred_design_pairs_equal_separate_calls(lbgpu, has_gpu, nz):
         b.adjoint_step(1, residual=False)
         assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
         assert np.array_equal(a.get_state(1), b.get_state(1))
+        # the upload buffer stays armed across other design writes
+        for k in range(3):
+            vals = rng.uniform(0.05, 1, a.n_design)
+            if k == 1:
+                for e in (a, b):
+                    e.primal_step_with_design(vals, 2, residual=False)
+                vals = rng.uniform(0.05, 1, a.n_design)
+            ja = a.pair_step_with_design(vals, residual=False)[2]
+            b.primal_step_with_design(vals, 1, residual=False)
+            b.adjoint_step(1, residual=False)
+            assert ja == b.objective()
+        a.finish()
+        assert np.array_equal(a.get_state(0), b.get_state(0))
+        assert np.array_equal(a.get_state(1), b.get_state(1))
 
 
 @pytest.mark.parametrize("name", list(CASES))

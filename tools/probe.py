@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Development probes on the GPU box (not the bench contract; bench.py is).
 
-  python tools/probe.py rates [C3 overrides key=value ...]
+  python tools/probe.py rates [C3 overrides key=value ...] [streaming=aa]
       sweep / pair rates of one C3 variant (CUDA events)
   python tools/probe.py geom
       fused-pair rate with and without pressure faces (tags.geometry=periodic)
@@ -14,7 +14,9 @@
   python tools/probe.py e2e
       lbgpu_pair_step_with_design rate (with LBGPU_TRACE_PAIR=1 in the
       environment, each call's stage timeline on stderr)
-  python tools/probe.py ncu {pair,sweeps,gradient,aa,e2e}
+  python tools/probe.py l2gran
+      objective / pair / e2e rates under each cudaLimitMaxL2FetchGranularity
+  python tools/probe.py ncu {pair,sweeps,gradient,aa,e2e,sweeps32}
       a short run to put under ncu
 """
 from __future__ import annotations
@@ -69,8 +71,10 @@ def kv(args):
 
 def main():
     cmd = sys.argv[1] if len(sys.argv) > 1 else "rates"
-    if cmd == "rates":
-        print(json.dumps(rates(kv(sys.argv[2:]))), flush=True)
+    if cmd == "rates":  # streaming=aa selects the in-place engine
+        ov = kv(sys.argv[2:])
+        st = ov.pop("streaming", "double")
+        print(json.dumps(rates(ov, streaming=st)), flush=True)
     elif cmd == "geom":
         for ov in ({}, {"tags.geometry": "periodic"}):
             print(json.dumps(rates(ov)), flush=True)
@@ -98,6 +102,45 @@ def main():
         e.finish()
         dt = (time.perf_counter() - t0) / K
         print(json.dumps({"e2e_ms_per_step": dt * 1e3, "e2e_mlups": e.n / dt / 1e6}), flush=True)
+    elif cmd == "l2gran":  # cudaLimitMaxL2FetchGranularity vs the objective / pair / e2e
+        import ctypes
+        import time
+        import torch
+        torch.cuda.init()
+        rt = None
+        for name in ("libcudart.so.12", "libcudart.so"):
+            try:
+                rt = ctypes.CDLL(name)
+                break
+            except OSError:
+                pass
+        e = _engine()
+        w = torch.from_numpy(e.design_values()).pin_memory().numpy()
+        for gran in (None, 32, 64, 128):
+            if gran is not None:
+                r = rt.cudaDeviceSetLimit(0x05, ctypes.c_size_t(gran))
+                assert r == 0, r
+            v = ctypes.c_size_t(0)
+            rt.cudaDeviceGetLimit(ctypes.byref(v), 0x05)
+            for _ in range(20):
+                e.objective()
+            t0 = time.perf_counter()
+            for _ in range(200):
+                e.objective()
+            tobj = (time.perf_counter() - t0) / 200
+            e.time_pair_steps(5)
+            tpair = e.time_pair_steps(50)
+            for _ in range(20):
+                e.pair_step_with_design(w, residual=False)
+            e.finish()
+            t0 = time.perf_counter()
+            for _ in range(200):
+                e.pair_step_with_design(w, residual=False)
+            e.finish()
+            dt = (time.perf_counter() - t0) / 200
+            print(json.dumps({"gran": v.value, "objective_us": tobj * 1e6,
+                              "pair_mlups": e.n * 50 / tpair / 1e3, "e2e_mlups": e.n / dt / 1e6}),
+                  flush=True)
     elif cmd == "ncu":
         what = sys.argv[2]
         if what == "pair":
@@ -112,6 +155,9 @@ def main():
             e.one_shot(np.full(3, 1e-4), np.zeros(3), record_interval=100)
         elif what == "aa":
             e = _engine(streaming="aa")
+            e.pair_steps(4, residual=False)
+        elif what == "sweeps32":  # FP32 pairs run as the two sweeps apart
+            e = _engine({"model.precision": 32})
             e.pair_steps(4, residual=False)
         elif what == "e2e":
             e = _engine()
