@@ -497,6 +497,8 @@ struct lbgpu_engine {
       x0 = 0, span = gnx;
     }
     N = (long long)nx * ny * nz;
+    // the sweeps address nodes with 32-bit offsets (kernels.cuh Nbr)
+    if (N > 0x7fffffffll) throw Fail{LBGPU_E_CONFIG, "more than 2^31 - 1 nodes on one device: split into slabs"};
     dim = nz == 1 ? 2 : 3;
     mf = dim == 2 ? LatD2::MF : LatD3::MF;
     mt = dim == 2 ? LatD2::MT : LatD3::MT;

@@ -40,9 +40,12 @@ LBGPU_HD long long gflat(const Geom& g, int x, int y, int z) {
 // Neighbour coordinate tables with periodic wrap on every axis of the local
 // array (primal_step's modular wrap, collision.cpp:343-351). Slab runs never
 // wrap in x because their computed columns exclude the ghost columns.
+// Node offsets are 32-bit (the engine holds N < 2^31 nodes per device): each
+// population address is then the plane's base (buf + P N, warp-uniform, in
+// uniform registers) plus one 32-bit offset -- one IMAD.WIDE per access
+// instead of a chain of 64-bit adds.
 struct Nbr {
-  int xs[3];
-  long long ys[3], zs[3];
+  int xs[3], ys[3], zs[3];
 };
 __device__ __forceinline__ Nbr make_nbr(const Geom& g, int x, int y, int z) {
   Nbr n;
@@ -51,10 +54,10 @@ __device__ __forceinline__ Nbr make_nbr(const Geom& g, int x, int y, int z) {
   n.xs[2] = x == g.nx - 1 ? 0 : x + 1;
   const int ym = y == 0 ? g.ny - 1 : y - 1, yp = y == g.ny - 1 ? 0 : y + 1;
   const int zm = z == 0 ? g.nz - 1 : z - 1, zp = z == g.nz - 1 ? 0 : z + 1;
-  n.ys[0] = (long long)g.nx * ym;
-  n.ys[1] = (long long)g.nx * y;
-  n.ys[2] = (long long)g.nx * yp;
-  const long long pl = (long long)g.nx * g.ny;
+  n.ys[0] = g.nx * ym;
+  n.ys[1] = g.nx * y;
+  n.ys[2] = g.nx * yp;
+  const int pl = g.nx * g.ny;
   n.zs[0] = pl * zm;
   n.zs[1] = pl * z;
   n.zs[2] = pl * zp;
@@ -62,15 +65,27 @@ __device__ __forceinline__ Nbr make_nbr(const Geom& g, int x, int y, int z) {
 }
 // Node index of x + D*e_P (D = -1: primal pull source, +1: adjoint pull source).
 template <class L, int P, int D>
-__device__ __forceinline__ long long nbr_idx(const Nbr& n) {
+__device__ __forceinline__ int nbr_idx(const Nbr& n) {
   constexpr int ex = D * cvel<L>(P, 0), ey = D * cvel<L>(P, 1), ez = D * cvel<L>(P, 2);
   return n.xs[1 + ex] + n.ys[1 + ey] + n.zs[1 + ez];
+}
+// Population P of node i: plane base first (uniform), then the node offset.
+#ifndef LBGPU_OFF32
+#define LBGPU_OFF32 0
+#endif
+template <class R>
+__device__ __forceinline__ R* pop(R* buf, long long N, int P, int i) {
+#if LBGPU_OFF32  // experiment: 32-bit element offsets (M N < 2^32)
+  return buf + (unsigned)((unsigned)P * (unsigned)N + (unsigned)i);
+#else
+  return (buf + P * N) + i;
+#endif
 }
 
 template <class L, class R, int D>
 __device__ __forceinline__ void gather(const R* __restrict__ buf, long long N, const Nbr& n,
                                        R* out) {
-  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(buf + P * N + nbr_idx<L, P, D>(n)); });
+  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(pop(buf, N, P, nbr_idx<L, P, D>(n))); });
 }
 
 // Split adjoint: stage the v gather through shared memory (see adjoint_body).
@@ -96,7 +111,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <class L, class R, int D>
 __device__ __forceinline__ void gather_async(const R* __restrict__ buf, long long N, const Nbr& n,
                                              R* smem, int stride) {
-  LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, buf + P * N + nbr_idx<L, P, D>(n)); });
+  LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, pop(buf, N, P, nbr_idx<L, P, D>(n))); });
   cp_async_commit();
 }
 
@@ -116,28 +131,29 @@ __device__ __forceinline__ void gather_async(const R* __restrict__ buf, long lon
 // the memory. D = -1 for the primal field, +1 for the adjoint (which streams
 // against the links, adjoint.cpp:239-249).
 enum : int { FM_DB = 0, FM_O = 1, FM_E = 2 };
-template <class L, int D, int FM, int P>
-__device__ __forceinline__ long long in_off(long long N, long long idx, const Nbr& n) {
-  if constexpr (FM == FM_DB) return P * N + nbr_idx<L, P, D>(n);
-  else if constexpr (FM == FM_O) return P * N + idx;
-  else return copp<L>(P) * N + nbr_idx<L, P, D>(n);
+// where node idx reads its pre-collision population P / writes its post value P
+template <class L, int D, int FM, int P, class R>
+__device__ __forceinline__ R* in_at(R* buf, long long N, long long idx, const Nbr& n) {
+  if constexpr (FM == FM_DB) return pop(buf, N, P, nbr_idx<L, P, D>(n));
+  else if constexpr (FM == FM_O) return pop(buf, N, P, int(idx));
+  else return pop(buf, N, copp<L>(P), nbr_idx<L, P, D>(n));
 }
-template <class L, int D, int FM, int P>
-__device__ __forceinline__ long long out_off(long long N, long long idx, const Nbr& n) {
-  if constexpr (FM == FM_DB) return P * N + idx;
-  else if constexpr (FM == FM_O) return copp<L>(P) * N + idx;
-  else return P * N + nbr_idx<L, P, -D>(n);
+template <class L, int D, int FM, int P, class R>
+__device__ __forceinline__ R* out_at(R* buf, long long N, long long idx, const Nbr& n) {
+  if constexpr (FM == FM_DB) return pop(buf, N, P, int(idx));
+  else if constexpr (FM == FM_O) return pop(buf, N, copp<L>(P), int(idx));
+  else return pop(buf, N, P, nbr_idx<L, P, -D>(n));
 }
 // gather of the pre-collision populations of node idx under mode FM
 template <class L, class R, int D, int FM>
 __device__ __forceinline__ void gather_m(const R* buf, long long N, long long idx, const Nbr& n,
                                          R* out) {
-  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(buf + in_off<L, D, FM, P>(N, idx, n)); });
+  LBGPU_FOR(P, 0, L::M, { out[P] = __ldg(in_at<L, D, FM, P>(buf, N, idx, n)); });
 }
 template <class L, class R, int D, int FM>
 __device__ __forceinline__ void gather_async_m(const R* buf, long long N, long long idx,
                                                const Nbr& n, R* smem, int stride) {
-  LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, buf + in_off<L, D, FM, P>(N, idx, n)); });
+  LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, in_at<L, D, FM, P>(buf, N, idx, n)); });
   cp_async_commit();
 }
 // in-place store of node idx's post-collision values (FM_O / FM_E)
@@ -145,7 +161,7 @@ template <class L, class R, int D, int FM>
 __device__ __forceinline__ void store_aa(R* buf, long long N, long long idx, const Nbr& n,
                                          const R* v) {
   static_assert(FM != FM_DB, "double-buffered stores go through store_node");
-  LBGPU_FOR(P, 0, L::M, { buf[out_off<L, D, FM, P>(N, idx, n)] = v[P]; });
+  LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, n) = v[P]; });
 }
 
 // Planes that cross a slab cut for a sweep pulling along D (-1 primal, +1
@@ -803,11 +819,11 @@ __device__ __forceinline__ void store_node(const R* __restrict__ src, R* __restr
                                            long long N, long long idx, const R* in,
                                            const R* out, unsigned long long& rmax,
                                            bool in_valid = true) {
-  LBGPU_FOR(P, 0, L::M, { dst[P * N + idx] = out[P]; });
+  LBGPU_FOR(P, 0, L::M, { *pop(dst, N, P, int(idx)) = out[P]; });
   if constexpr (RESID) {
     LBGPU_FOR(P, 0, L::M, {
       constexpr bool rest = cvel<L>(P, 0) == 0 && cvel<L>(P, 1) == 0 && cvel<L>(P, 2) == 0;
-      const R old = (rest && in_valid) ? in[P] : __ldg(src + P * N + idx);
+      const R old = (rest && in_valid) ? in[P] : __ldg(pop(src, N, P, int(idx)));
       const unsigned long long d = absdiff_bits(double(out[P]), double(old));
       rmax = d > rmax ? d : rmax;
     });
@@ -993,8 +1009,11 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 #ifndef LBGPU_AA_PRIMAL_MINB
 #define LBGPU_AA_PRIMAL_MINB 3
 #endif
+#ifndef LBGPU_AA_PRIMAL_MINB32
+#define LBGPU_AA_PRIMAL_MINB32 1
+#endif
 template <class L, class R, int CK, int FM>
-__global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : 1)
+__global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : LBGPU_AA_PRIMAL_MINB32)
     k_primal_aa(Launch a, R* A, int c0, int c1) {
   unsigned long long rmax = 0;
   if (c0 >= 0) {
@@ -1233,9 +1252,12 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
 #ifndef LBGPU_AA_ADJ_MINB
 #define LBGPU_AA_ADJ_MINB 3
 #endif
+#ifndef LBGPU_AA_ADJ_MINB32
+#define LBGPU_AA_ADJ_MINB32 LBGPU_ADJ_MINB32
+#endif
 template <class L, class R, int CK, int BM, int VM, bool MOM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_ADJ_MINB
-                                                      : (MOM ? LBGPU_ADJ_MINB32_MOM : LBGPU_ADJ_MINB32))
+                                                      : (MOM ? LBGPU_ADJ_MINB32_MOM : LBGPU_AA_ADJ_MINB32))
     k_adjoint_aa(Launch a, const R* __restrict__ base,
                                                             R* V, const R* __restrict__ mom,
                                                             int c0, int c1) {
@@ -1541,8 +1563,17 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair_cols(Launch a, const R* __restrict__
 // each updated in place; COLS as k_primal_aa. The side-list adjoint nodes run
 // BEFORE it (k_adjoint_side reads the base f^{n+1} that this kernel
 // overwrites; their v locations are theirs alone).
+#ifndef LBGPU_AAPAIR_MINB
+#define LBGPU_AAPAIR_MINB LBGPU_PAIR_MINB
+#endif
+#ifndef LBGPU_AAPAIR_MINB32
+#define LBGPU_AAPAIR_MINB32 LBGPU_PAIR_MINB32
+#endif
 template <class L, class R, int CK, int FM, int VM>
-__global__ void LBGPU_PAIR_BOUNDS(R) k_pair_aa(Launch a, R* F, R* V, int c0, int c1) {
+__global__ void __launch_bounds__(kPairThreads<R>,
+                                  (sizeof(R) == 4 ? LBGPU_AAPAIR_MINB32 : LBGPU_AAPAIR_MINB) * 128 /
+                                      kPairThreads<R>)
+    k_pair_aa(Launch a, R* F, R* V, int c0, int c1) {
   unsigned long long rP = 0, rA = 0;
   if (c0 >= 0) {
     const long long yz = (long long)a.g.ny * a.g.nz;
@@ -1771,7 +1802,7 @@ __global__ void k_layout(Geom g, const void* __restrict__ in, void* __restrict__
   if constexpr (TO_REF) {
     const R* post = static_cast<const R*>(in);
     double* ref = static_cast<double*>(out);
-    LBGPU_FOR(P, 0, L::M, { ref[P * N + idx] = double(post[in_off<L, D, FM, P>(N, idx, nb)]); });
+    LBGPU_FOR(P, 0, L::M, { ref[P * N + idx] = double(*in_at<L, D, FM, P>(post, N, idx, nb)); });
   } else {
     const double* ref = static_cast<const double*>(in);
     R* post = static_cast<R*>(out);
@@ -2150,6 +2181,10 @@ void adjoint_aa(const SweepArgs& s, const void* base, void* V) {
 }
 #endif
 #if defined(LBGPU_PART_AAPAIR)
+// Block width of the in-place pair (rows of the block along x).
+#ifndef LBGPU_AAPAIR_BX
+#define LBGPU_AAPAIR_BX LBGPU_PAIR_BX
+#endif
 void pair_aa(const SweepArgs& s, void* F, void* V) {
 #if !LBGPU_EXACT
   LBGPU_LR_DISPATCH(s.dim, s.prec, LBGPU_CK_DISPATCH({
@@ -2177,7 +2212,7 @@ void pair_aa(const SweepArgs& s, void* F, void* V) {
       if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
       if (a.g.x1 <= a.g.x0) return;
       const int wx = a.g.x1 - a.g.x0;
-      const int bx = wx >= LBGPU_PAIR_BX ? LBGPU_PAIR_BX : (wx >= 64 ? 64 : 32);
+      const int bx = wx >= LBGPU_AAPAIR_BX ? LBGPU_AAPAIR_BX : (wx >= 64 ? 64 : 32);
       const int by = TB / bx;
       dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, a.g.nz);
       k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v, -1, -1);
