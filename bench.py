@@ -371,8 +371,9 @@ def main() -> None:
         # order, 16 MB at C3) H2D from pinned memory, one primal sweep, one
         # adjoint sweep against the new state, J of the new state back to the
         # host. Each call's adjoint sweep is deferred into the next call's
-        # fused sweep (z-chunks gated on the upload slices); the timed region
-        # ends with lbgpu_finish, which runs the last one. A benchmark
+        # fused sweep (each design node's thread waits for its own uploaded
+        # value); the timed region ends with lbgpu_finish, which runs the last
+        # one. A benchmark
         # composite of the reference's operators.
         def e2e_step():
             return eng.pair_step_with_design(w_np, residual=False)[2]
@@ -382,6 +383,7 @@ def main() -> None:
             eng.adjoint_step(1, residual=False)
             return eng.objective()
         path = "lbgpu_pair_step_with_design(pinned host w; J to the host)"
+        d2h = 48  # one read per call: J and the call's five status words
     else:
         # in place / slabs: lbgpu_set_design_values (H2D of this rank's design
         # values), lbgpu_pair_steps(1), lbgpu_objective (J to the host)
@@ -391,6 +393,7 @@ def main() -> None:
             return eng.objective()
         e2e_step_apart = None
         path = "lbgpu_set_design_values + lbgpu_pair_steps(1) + lbgpu_objective"
+        d2h = 8 + 32  # lbgpu_objective: J, then the status words
 
     def e2e_time(fn, steps, warm, gap_s=0.0):
         """Wall time per call; with gap_s the host idles that long between
@@ -422,8 +425,7 @@ def main() -> None:
     e2e_steps = args.e2e_steps if world == 1 else min(args.e2e_steps, 30)
     e2e = {"value": e2e_time(e2e_step, e2e_steps, max(args.warmup, 30 if world == 1 else 3)),
            "unit": "MLUPS",
-           # J (8 B) + the call's status words (4 x 8 B)
-           "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": 8 + 32,
+           "h2d_bytes_per_step": int(8 * eng.n_design), "d2h_bytes_per_step": d2h,
            "steps": e2e_steps, "path": path,
            "regime": "back-to-back calls from one pinned host buffer (steady state)"}
     if world == 1:

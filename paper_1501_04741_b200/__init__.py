@@ -161,6 +161,7 @@ class Engine:
         self.shape = (dims[0], dims[1], dims[2])
         self.m, self.mf, self.mt, self.precision, self.exact = dims[3], dims[4], dims[5], dims[6], dims[7]
         self.n, self.n_design, self.n_support, self.n_inlets = cnt[0], cnt[1], cnt[2], cnt[3]
+        self._wd_cache = (None, None)  # (design buffer, its address): pair_step_with_design
 
     # --- construction -------------------------------------------------------
     @classmethod
@@ -329,10 +330,12 @@ class Engine:
         overlapped pipeline. Returns (primal_residual, adjoint_residual, J),
         None where not requested."""
         w_design = np.ascontiguousarray(w_design, np.float64)
-        assert w_design.size == self.n_design
+        if self._wd_cache[0] is not w_design:  # one optimizer buffer, reused every call
+            assert w_design.size == self.n_design
+            self._wd_cache = (w_design, _ptr(w_design))
         rp, ra, j = C.c_double(), C.c_double(), C.c_double()
         self._ok(self.L.lbgpu_pair_step_with_design(
-            self.h, _ptr(w_design), C.byref(rp) if residual else None,
+            self.h, self._wd_cache[1], C.byref(rp) if residual else None,
             C.byref(ra) if residual else None, C.byref(j) if objective else None))
         return (rp.value if residual else None, ra.value if residual else None,
                 j.value if objective else None)

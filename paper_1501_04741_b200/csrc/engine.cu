@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -165,7 +166,8 @@ void model_rows(std::vector<double>& U, std::vector<int>& cls) {
 // one block with a barrier per level.
 __global__ void __launch_bounds__(1024) k_tree_small(const double* __restrict__, const long long* __restrict__,
                              const long long* __restrict__, int, const int2* __restrict__,
-                             const int* __restrict__, int, int, double*);
+                             const int* __restrict__, int, int, double*, unsigned long long*,
+                             unsigned long long*);
 struct PairTree {
   static constexpr int kTopOps = 2048;  // levels narrower than this: single-block kernel
   static constexpr size_t kSmallMax = 160 * 1024;  // whole tree in one block's shared memory
@@ -282,7 +284,8 @@ __global__ void __launch_bounds__(1024) k_tree_small(const double* __restrict__ 
                                                      const long long* __restrict__ hi, int leaves,
                                                      const int2* __restrict__ ops,
                                                      const int* __restrict__ lvl, int levels,
-                                                     int nops, double* out) {
+                                                     int nops, double* out, unsigned long long* fl,
+                                                     unsigned long long* pub) {
   extern __shared__ double sv[];  // [leaves + ops] values, then the ops, then lvl
   int2* sop = reinterpret_cast<int2*>(sv + leaves + nops);
   int* slv = reinterpret_cast<int*>(sop + nops);
@@ -308,7 +311,17 @@ __global__ void __launch_bounds__(1024) k_tree_small(const double* __restrict__ 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = nops ? sv[leaves + nops - 1] : sv[0];
+  if (threadIdx.x == 0) {
+    const double J = nops ? sv[leaves + nops - 1] : sv[0];
+    *out = J;
+    if (pub) {  // the call's last kernel: its status words and J straight to
+                // mapped host memory, then the words' start values (no D2H
+                // copy, no reset launch before the next call)
+      for (int i = 0; i < 6; ++i)
+        pub[i] = i == 4 ? (unsigned long long)__double_as_longlong(J) : fl[i];
+      for (int i = 0; i < 6; ++i) fl[i] = (i == 1 || i == 3) ? kNoBad : 0ull;
+    }
+  }
 }
 
 // The flag words' start values (a kernel: no pageable-memory copy per call).
@@ -417,6 +430,8 @@ struct lbgpu_engine {
   unsigned long long* d_flags = nullptr;
   unsigned long long* d_ring = nullptr;   // per-step residual ring for batched solves
   unsigned long long* h_flags = nullptr;  // pinned mirror
+  volatile unsigned long long* h_pub = nullptr;  // mapped: words published by k_tree_small
+  unsigned long long* d_pub = nullptr;           // its device address
   PairTree tree_support, tree_design, tree_inlet;
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -456,6 +471,7 @@ struct lbgpu_engine {
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
+    if (h_pub) cudaFreeHost(const_cast<unsigned long long*>(h_pub));
     tree_support.release(), tree_design.release(), tree_inlet.release();
     for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     for (cudaEvent_t ev : trace_ev) cudaEventDestroy(ev);
@@ -590,6 +606,12 @@ struct lbgpu_engine {
     CU(cudaMalloc(&d_flags, sizeof(unsigned long long) * 6));
     CU(cudaMalloc(&d_ring, sizeof(unsigned long long) * kRing));
     CU(cudaMallocHost(&h_flags, sizeof(unsigned long long) * (4 + kRing)));
+    {
+      void* hp = nullptr;
+      CU(cudaHostAlloc(&hp, sizeof(unsigned long long) * 8, cudaHostAllocMapped));
+      h_pub = static_cast<volatile unsigned long long*>(hp);
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pub), hp, 0));
+    }
     tree_support.build((long long)support.size());
     tree_design.build((long long)design.size());
     tree_inlet.build((long long)inlets.size());
@@ -732,12 +754,18 @@ struct lbgpu_engine {
   // ------------------------------------------------------------ helpers
   // d_flags: [0] residual, [1] first bad node (primal, or the call's only
   // sweep kind), [2] aux, [3] first bad node of the adjoint half of a pair call
+  // flags_clean: the last flag-touching operation was a design pair whose
+  // final kernel published and reset the words (k_tree_small), so the next
+  // reset needs no launch. Any reset or Launch clears it.
+  mutable bool flags_clean = false;
   void reset_flags() {
-    k_reset_flags<<<1, 32, 0, st>>>(d_flags);
+    if (!flags_clean) k_reset_flags<<<1, 32, 0, st>>>(d_flags);
+    flags_clean = false;
     kb_p = primal_steps, kb_a = adjoint_steps, kb_t = tangent_steps;
   }
   // step: the sweep's number relative to the current key base (1-based)
   Launch launch(unsigned long long step) const {
+    flags_clean = false;
     Launch a;
     a.g = G;
     a.t = T;
@@ -1049,6 +1077,11 @@ struct lbgpu_engine {
   // LBGPU_TRACE_PAIR=1: print each pipeline stage's finish time (development).
   std::vector<cudaEvent_t> trace_ev;
   std::vector<std::string> trace_name;
+  std::vector<double> trace_host;  // host clock at each mark (us)
+  double trace_t_exit = 0.0;       // host clock when the previous traced call returned
+  static double host_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   static bool trace_on() {
     static const bool on = std::getenv("LBGPU_TRACE_PAIR") != nullptr;
     return on;
@@ -1061,17 +1094,26 @@ struct lbgpu_engine {
     }
     CU(cudaEventRecord(trace_ev[trace_name.size()], s_));
     trace_name.emplace_back(what);
+    trace_host.push_back(host_us());
   }
+  // one line per call: each mark's GPU time (ms after "start"), the host
+  // clock of its enqueue (us after "start"), the host's return from the sync,
+  // and the host gap since the previous traced call returned
   void trace_print() {
     if (trace_name.empty()) return;
+    const double t_sync = host_us();
     CU(cudaDeviceSynchronize());
     for (size_t i = 1; i < trace_name.size(); ++i) {
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, trace_ev[0], trace_ev[i]));
-      std::fprintf(stderr, "%s %.3f  ", trace_name[i].c_str(), ms);
+      std::fprintf(stderr, "%s %.3f (host +%.1f)  ", trace_name[i].c_str(), ms,
+                   trace_host[i] - trace_host[0]);
     }
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, "synced host +%.1f  gap_before_call %.1f\n", t_sync - trace_host[0],
+                 trace_t_exit > 0 ? trace_host[0] - trace_t_exit : 0.0);
     trace_name.clear();
+    trace_host.clear();
+    trace_t_exit = host_us();
   }
   void design_pair(const double* wd, double* rp, double* ra, double* J) {
     require_solo();
@@ -1094,7 +1136,7 @@ struct lbgpu_engine {
     int zb[kChunks + 1];
     reset_flags();
     CU(cudaMemsetAsync(d_ring, 0, sizeof(unsigned long long), st));
-    trace_name.clear();  // a call that raised before trace_print left its names
+    trace_name.clear(), trace_host.clear();  // a call that raised before trace_print left its names
     trace("start", st);
     ensure_h2d();
     CU(cudaEventRecord(ev_chunk[kChunks], st));  // everything before this call
@@ -1260,12 +1302,13 @@ struct lbgpu_engine {
     adj_pending = false;
     long long ib[kChunks + 1];
     int zb[kChunks + 1];
-    reset_flags();
-    trace_name.clear();
+    trace_name.clear(), trace_host.clear();
     trace("start", st);
+    reset_flags();
     ++primal_steps;
     if (fuse) ++adjoint_steps;
     const bool gated = fuse && gate_ready();
+    bool published = false;
     if (gated) {
       gated_pair(wd);
     } else {
@@ -1305,19 +1348,23 @@ struct lbgpu_engine {
       fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support,
                             (long long)support.size(), d_terms, 0);
       ++launches;
-      pairwise_queue(tree_support, d_terms, reinterpret_cast<double*>(d_flags + 4));
+      published = pairwise_queue(tree_support, d_terms, reinterpret_cast<double*>(d_flags + 4), true);
       if (trace_on()) trace("J", st);
     }
     CU(cudaGetLastError());
     reduce_flags(d_flags + 1, 1, true);
-    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
+    if (!published)
+      CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
     sync();  // one host sync per call; the host design buffer is consumed too
+    if (published)
+      for (int i = 0; i < 6; ++i) h_flags[i] = h_pub[i];
     trace_print();
     if (gated && !h_flags[5]) gate_armed = true;
     if (gated && h_flags[5])
       throw Fail{LBGPU_E_NUMERIC, "design upload: a slice did not land within the sweep's wait bound"};
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], fuse ? "iteration (or the deferred adjoint iteration)" : "iteration");
     adj_pending = true;
+    flags_clean = published;
     if (J) *J = bits_to_double(h_flags[4]);
   }
 
@@ -1836,13 +1883,16 @@ struct lbgpu_engine {
     return out;
   }
   // the tree replay only; the sum lands in *out (default d_scalar[0])
-  void pairwise_queue(PairTree& tr, const double* d_t, double* out = nullptr) {
+  // publish: also copy the status words and the sum to h_pub (mapped) and
+  // reset the words -- one-block trees only; returns whether it did
+  bool pairwise_queue(PairTree& tr, const double* d_t, double* out = nullptr, bool publish = false) {
     if (!out) out = d_scalar;
     if (tr.small()) {
       k_tree_small<<<1, 1024, tr.small_bytes, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_ops, tr.d_lvl,
-                                                     int(tr.lvl.size()) - 1, tr.ops, out);
+                                                     int(tr.lvl.size()) - 1, tr.ops, out, d_flags,
+                                                     publish ? d_pub : nullptr);
       ++launches;
-      return;
+      return publish;
     }
     const int nb = (tr.leaves + 127) / 128;
     k_leaf_sums<<<nb, 128, 0, st>>>(d_t, tr.d_lo, tr.d_hi, tr.leaves, tr.d_vals);
@@ -1853,6 +1903,7 @@ struct lbgpu_engine {
     k_combine_top<<<1, 1024, 0, st>>>(tr.d_vals, tr.d_ops, tr.d_lvl, tr.leaves, tr.top,
                                       int(tr.lvl.size()) - 1, tr.ops, out);
     launches += 2 + tr.top;
+    return false;
   }
   double objective(const void* buf = nullptr) {
     const Launch a = launch(primal_steps - kb_p);

@@ -70,16 +70,11 @@ __device__ __forceinline__ int nbr_idx(const Nbr& n) {
   return n.xs[1 + ex] + n.ys[1 + ey] + n.zs[1 + ez];
 }
 // Population P of node i: plane base first (uniform), then the node offset.
-#ifndef LBGPU_OFF32
-#define LBGPU_OFF32 0
-#endif
+// (32-bit element offsets P N + i, valid while M N < 2^32, measured mixed on
+// B200 C3: FP32 in-place adjoint +4%, the FP64 fused pair -5%; not used.)
 template <class R>
 __device__ __forceinline__ R* pop(R* buf, long long N, int P, int i) {
-#if LBGPU_OFF32  // experiment: 32-bit element offsets (M N < 2^32)
-  return buf + (unsigned)((unsigned)P * (unsigned)N + (unsigned)i);
-#else
   return (buf + P * N) + i;
-#endif
 }
 
 template <class L, class R, int D>
@@ -91,6 +86,9 @@ __device__ __forceinline__ void gather(const R* __restrict__ buf, long long N, c
 // Split adjoint: stage the v gather through shared memory (see adjoint_body).
 #ifndef LBGPU_ADJ_STAGE
 #define LBGPU_ADJ_STAGE 1
+#endif
+#ifndef LBGPU_ADJ_STAGE32  // the FP32 split adjoint too
+#define LBGPU_ADJ_STAGE32 0
 #endif
 
 // Asynchronous gather into shared memory (cp.async, LDGSTS): the loads are
@@ -1009,8 +1007,9 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 #ifndef LBGPU_AA_PRIMAL_MINB
 #define LBGPU_AA_PRIMAL_MINB 3
 #endif
+// FP32, 1/4/6/8 blocks per SM: 5,276 / 5,326 / 5,036 / 4,690 GB/s.
 #ifndef LBGPU_AA_PRIMAL_MINB32
-#define LBGPU_AA_PRIMAL_MINB32 1
+#define LBGPU_AA_PRIMAL_MINB32 4
 #endif
 template <class L, class R, int CK, int FM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : LBGPU_AA_PRIMAL_MINB32)
@@ -1067,7 +1066,7 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
       // FP64: v's gather goes out first, through shared memory, so it overlaps
       // the base gather and the moment sums instead of following them
       // (C3 +0.5% gathering, +1.7% frozen base; FP32 measured slower: off)
-      constexpr bool kStage = LBGPU_ADJ_STAGE && sizeof(R) == 8;
+      constexpr bool kStage = LBGPU_ADJ_STAGE && (sizeof(R) == 8 || LBGPU_ADJ_STAGE32);
       __shared__ R vsm[kStage ? L::M * 128 : 1];
       R* my = vsm + (kStage ? threadIdx.x : 0);
       if constexpr (kStage) {
@@ -1252,8 +1251,9 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
 #ifndef LBGPU_AA_ADJ_MINB
 #define LBGPU_AA_ADJ_MINB 3
 #endif
+// FP32, 4/5/6/8 blocks per SM: 4,467 / 4,888 / 5,088 / 4,702 GB/s.
 #ifndef LBGPU_AA_ADJ_MINB32
-#define LBGPU_AA_ADJ_MINB32 LBGPU_ADJ_MINB32
+#define LBGPU_AA_ADJ_MINB32 6
 #endif
 template <class L, class R, int CK, int BM, int VM, bool MOM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_ADJ_MINB

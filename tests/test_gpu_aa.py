@@ -133,3 +133,27 @@ def test_aa_nccl_single_rank_ring_equals_monolithic(lbgpu, has_gpu, name):
         assert np.array_equal(owned(ring, 0), mono.get_state(0))
         assert np.array_equal(owned(ring, 1), mono.get_state(1))
     assert mono.objective() == ring.objective()
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_aa_bitwise_at_c3_size(lbgpu, has_gpu, prec):
+    """The in-place kernels at the bench config's own size (C3, 256x128x128,
+    4.2M nodes; FP32 is C5's one-GPU capacity mode): sweeps, frozen-base
+    adjoint, fused pairs from both layouts, the gradient and J, bitwise the
+    double-buffered engine."""
+    from paper_1501_04741_b200.presets import config_text
+    a, b = twins(lbgpu, config_text("C3", {"model.precision": prec}))
+    for k in (20, 1):
+        a.primal_step(k, residual=False)
+        b.primal_step(k, residual=False)
+    for k in (1, 4):
+        a.adjoint_step(k, residual=False)
+        b.adjoint_step(k, residual=False)
+    for k in (3, 4):
+        a.pair_steps(k, residual=False)
+        b.pair_steps(k, residual=False)
+    same(a, b)
+    ga, da = a.param_gradient()
+    gb, db = b.param_gradient()
+    assert np.array_equal(ga, gb) and da == db
+    assert a.objective() == b.objective()

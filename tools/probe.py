@@ -92,16 +92,18 @@ def main():
         import torch
         e = _engine()
         w = torch.from_numpy(e.design_values()).pin_memory().numpy()
-        for _ in range(40):
-            e.pair_step_with_design(w, residual=False)
-        e.finish()
-        K = 200
-        t0 = time.perf_counter()
-        for _ in range(K):
-            e.pair_step_with_design(w, residual=False)
-        e.finish()
-        dt = (time.perf_counter() - t0) / K
-        print(json.dumps({"e2e_ms_per_step": dt * 1e3, "e2e_mlups": e.n / dt / 1e6}), flush=True)
+        for obj in (True, False, True):  # J read back, or not
+            for _ in range(40):
+                e.pair_step_with_design(w, residual=False, objective=obj)
+            e.finish()
+            K = 200
+            t0 = time.perf_counter()
+            for _ in range(K):
+                e.pair_step_with_design(w, residual=False, objective=obj)
+            e.finish()
+            dt = (time.perf_counter() - t0) / K
+            print(json.dumps({"objective": obj, "e2e_ms_per_step": dt * 1e3,
+                              "e2e_mlups": e.n / dt / 1e6}), flush=True)
     elif cmd == "l2gran":  # cudaLimitMaxL2FetchGranularity vs the objective / pair / e2e
         import ctypes
         import time
