@@ -412,11 +412,12 @@ def test_deferred_design_pairs_equal_separate_calls(lbgpu, has_gpu, nz):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_frozen_base_moment_cache_is_bitwise(lbgpu, has_gpu, name):
+@pytest.mark.parametrize("prec", [64, 32])
+def test_frozen_base_moment_cache_is_bitwise(lbgpu, has_gpu, name, prec):
     """adjoint_step(n >= 2) and solve_adjoint cache the frozen base's moments
     (k_base_moments) instead of gathering the base every sweep; the adjoint
     states must equal single-sweep calls (which gather) bit for bit."""
-    txt = case_text(name)
+    txt = case_text(name, {"model.precision": prec})
     a = lbgpu.Engine.from_config(txt)
     b = lbgpu.Engine.from_config(txt)
     for e in (a, b):
