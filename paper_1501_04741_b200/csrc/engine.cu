@@ -1361,7 +1361,7 @@ struct lbgpu_engine {
     trace_print();
     if (gated && !h_flags[5]) gate_armed = true;
     if (gated && h_flags[5])
-      throw Fail{LBGPU_E_NUMERIC, "design upload: a slice did not land within the sweep's wait bound"};
+      throw Fail{LBGPU_E_NUMERIC, "design upload: a design value did not land within the sweep's wait bound"};
     if (h_flags[1] != kNoBad) raise_bad(h_flags[1], fuse ? "iteration (or the deferred adjoint iteration)" : "iteration");
     adj_pending = true;
     flags_clean = published;

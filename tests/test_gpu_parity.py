@@ -359,6 +359,41 @@ def test_pair_step_with_design_equals_separate_calls(lbgpu, has_gpu, nz):
             assert np.array_equal(a.param_gradient()[0], b.param_gradient()[0])
 
 
+def test_gated_upload_never_hangs(lbgpu, has_gpu):
+    """The gated fused sweep takes the sentinel bit pattern (kGateEmpty) as
+    "not landed yet": a design vector carrying it fails the call with
+    E_NUMERIC after the bounded wait instead of hanging, and the engine
+    recovers (re-armed upload buffer) once it is given a valid state."""
+    import time
+    txt = case_text("mix3d", {"lattice.nz": 16})
+    a = lbgpu.Engine.from_config(txt)
+    b = lbgpu.Engine.from_config(txt)
+    for e in (a, b):
+        e.init_state()
+        e.primal_step(10)
+    vals = np.random.default_rng(4).uniform(0.05, 1, a.n_design)
+    a.pair_step_with_design(vals, residual=False)  # leaves its adjoint sweep pending
+    bad = vals.copy()
+    bad.view(np.uint64)[a.n_design // 2] = np.uint64(0x7FF4DEAD0000BEEF)
+    t0 = time.time()
+    with pytest.raises(lbgpu.LbgpuError) as ex:
+        a.pair_step_with_design(bad, residual=False)  # gated: waits, then gives up
+    assert ex.value.code == lbgpu.E_NUMERIC and "upload" in ex.value.msg
+    assert time.time() - t0 < 30
+    for e in (a, b):
+        e.init_state()
+        e.set_design_values(vals)
+        e.primal_step(10)
+    for _ in range(3):
+        ja = a.pair_step_with_design(vals, residual=False)[2]
+        b.primal_step_with_design(vals, 1, residual=False)
+        b.adjoint_step(1, residual=False)
+        assert ja == b.objective()
+    a.finish()
+    assert np.array_equal(a.get_state(0), b.get_state(0))
+    assert np.array_equal(a.get_state(1), b.get_state(1))
+
+
 @pytest.mark.parametrize("nz", [16, 37])
 def test_deferred_design_pairs_equal_separate_calls(lbgpu, has_gpu, nz):
     """Back-to-back lbgpu_pair_step_with_design calls without residuals defer
