@@ -18,11 +18,12 @@ Workloads:
   x-slab per GPU of a (256 N)x128x128 lattice.
 * C5 (default at N > 1): the 2048x512x512 channel (536,870,912 nodes) split
   into N x-slabs (strong scaling, decompose, partition.cpp:9-21), halos over
-  NCCL overlapped with the interior columns. Capacity: the state is stored
-  in place (AA-pattern streaming, one buffer per field): FP64 at N >= 2
-  (111.7 GB of f + v per GPU at N = 2); at N = 1 the FP64 pair (223 GB) does
-  not fit a 180 GB B200, so N = 1 runs the reference's own precision = 32
-  mode (111.7 GB) and says so in "dtype" and "config.capacity".
+  NCCL overlapped with the interior columns. Capacity: FP64 double-buffered
+  at N >= 4 (115 GB of f, f', v, v' per GPU at N = 4); in place (AA-pattern
+  streaming, one buffer per field) at N = 2 (111.7 GB of f + v per GPU); at
+  N = 1 the FP64 pair (223 GB) does not fit a 180 GB B200, so N = 1 runs the
+  reference's own precision = 32 mode in place (111.7 GB) and says so in
+  "dtype" and "config.capacity".
 
 --gpus N > 1 launches the N ranks itself (torch.distributed.run) unless it is
 already running under one; it fails when fewer than N GPUs are visible.
@@ -141,13 +142,19 @@ def workload(args, world: int) -> dict:
                                 "exchange overlapped with interior columns") if world > 1 else "1 GPU",
                 "capacity": "double-buffered f and v (the reference's StateField layout)"}
     prec = 64 if world >= 2 else 32
-    return {"id": "C5", "txt": config_text("C5", {"model.precision": prec}), "streaming": "aa",
+    # the double buffer (f, f', v, v': 115 GB of FP64 per GPU at N = 4) where it
+    # fits, else in place (one buffer per field)
+    st = "double" if world >= 4 else "aa"
+    return {"id": "C5", "txt": config_text("C5", {"model.precision": prec}), "streaming": st,
             "scaling": "strong",
             "desc": ("C5: mixer3d 2048x512x512 (536,870,912 nodes) split over the GPUs, D3Q19+D3Q7 "
                      "FMRT, primal sweep + adjoint sweep per step"),
             "parallelism": (f"{world} x-slabs of 2048x512x512 (decompose), NCCL halo exchange "
                             "overlapped with interior columns") if world > 1 else "1 GPU",
-            "capacity": ("in-place AA streaming (one buffer per field), FP64" if prec == 64 else
+            "capacity": ("double-buffered f and v, FP64 (the reference's StateField layout)"
+                         if st == "double" else
+                         "in-place AA streaming (one buffer per field), FP64: the double buffer "
+                         "would need 223 GB per GPU" if prec == 64 else
                          "in-place AA streaming, FP32 (the reference's model.precision = 32): "
                          "the FP64 f + v pair is 223 GB, above one B200's 180 GB")}
 
