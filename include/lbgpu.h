@@ -200,9 +200,12 @@ int lbgpu_fd_gradient_batch(lbgpu_engine* e, int64_t n, const int64_t* ordinals,
                             int64_t fixed_iters, int from_state, double* out);
 /* optimizer.cpp:200-202: write new design values (DesignField::nodes order,
  * host memory; pinned overlaps best) into w, then n >= 1 primal steps. The
- * upload is pipelined under the first sweep in z-chunks. Equivalent to
- * lbgpu_set_design_values + lbgpu_primal_step; the buffer is consumed when the
- * call returns. residual (nullable) as lbgpu_primal_step. */
+ * upload overlaps the first sweep: one launch whose design nodes wait for
+ * their own values (3D product build, box-shaped design, no residual on the
+ * first sweep), else z-chunks. Equivalent to lbgpu_set_design_values +
+ * lbgpu_primal_step; the buffer is consumed when the call returns. residual
+ * (nullable) as lbgpu_primal_step. The gated form, like the design pair's,
+ * reads the bit pattern 0x7ff4dead0000beef as "not landed yet". */
 int lbgpu_primal_step_with_design(lbgpu_engine* e, const double* w_design, int64_t n,
                                   double* residual);
 /* A benchmark composite of the reference's operators (no reference loop runs

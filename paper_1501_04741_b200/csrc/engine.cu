@@ -1255,7 +1255,9 @@ struct lbgpu_engine {
   // Enqueueing the copy first keeps the scheme deadlock-free where launches
   // serialise with copies (CUDA_LAUNCH_BLOCKING, profilers): the values are
   // then in place when the sweep starts.
-  void gated_pair(const double* wd) {
+  // The upload of a gated sweep (copy stream); the caller launches the sweep
+  // next and sets gate_armed again once its flags show no timeout.
+  void gate_upload(const double* wd) {
     ensure_h2d();
     const long long n = (long long)design.size();
     if (!gate_armed) {  // first use, or after a timed-out upload
@@ -1267,6 +1269,9 @@ struct lbgpu_engine {
     CU(cudaStreamWaitEvent(st_h2d, ev_chunk[kChunks], 0));
     CU(cudaMemcpyAsync(d_wgate, wd, sizeof(double) * n, cudaMemcpyHostToDevice, st_h2d));
     gate_armed = false;  // until the sweep is known to have re-armed every entry
+  }
+  void gated_pair(const double* wd) {
+    gate_upload(wd);
     NodeTables tn = T;
     tn.w = d_w2;     // the new design's full-grid buffer (design nodes written by the sweep)
     tn.w_adj = d_w;  // the previous design (the deferred adjoint half)
@@ -1385,13 +1390,37 @@ struct lbgpu_engine {
       return steps(0, nsteps, 0, want_resid);
     }
     if (nsteps <= 0) return 0.0;
+    const bool r0 = want_resid && nsteps == 1;
+    if (!r0 && gate_ready()) {
+      // box-shaped design: ONE primal launch behind ONE copy, each design
+      // node's thread waiting for its own value (the design pair's gate)
+      reset_flags();
+      ++primal_steps;
+      gate_upload(wd);
+      SweepArgs sa = sweep(primal_steps - kb_p, false, nullptr);
+      sa.a.gate = gate_box;
+      sa.a.gate.wd = d_wgate, sa.a.gate.w_out = d_w;  // == T.w: the sweep reads it back
+      sa.a.gate.err = reinterpret_cast<unsigned*>(d_flags + 5);
+      fast::primal(sa, f[fc], f[1 - fc]);
+      ++launches;
+      fc ^= 1;
+      w_host_stale = true;
+      for (long long k = 1; k < nsteps; ++k) primal_launch(want_resid && k == nsteps - 1, nullptr);
+      CU(cudaGetLastError());
+      CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
+      sync();  // also: the host buffer has been consumed when we return
+      if (h_flags[5])
+        throw Fail{LBGPU_E_NUMERIC, "design upload: a design value did not land within the sweep's wait bound"};
+      gate_armed = true;
+      if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+      return want_resid ? bits_to_double(h_flags[0]) : 0.0;
+    }
     long long ib[kChunks + 1];
     int zb[kChunks + 1];
     reset_flags();
     queue_design_upload(wd, ib, zb);
     ++primal_steps;
     ++launches;
-    const bool r0 = want_resid && nsteps == 1;
     for (int c = 0; c < kChunks; ++c) {
       const long long m_ = ib[c + 1] - ib[c];
       if (m_ > 0) {
@@ -1912,9 +1941,12 @@ struct lbgpu_engine {
     if (exact) exact::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, bm);
     else fast::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, bm);
     CU(cudaGetLastError());
-    const double val = pairwise(tree_support, d_terms);
-    check_bad("iteration");
-    return val;
+    // J lands next to the status words: one readback, one host sync
+    pairwise_queue(tree_support, d_terms, reinterpret_cast<double*>(d_flags + 4));
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned long long) * 5, cudaMemcpyDeviceToHost, st));
+    sync();
+    if (h_flags[1] != kNoBad) raise_bad(h_flags[1], "iteration");
+    return bits_to_double(h_flags[4]);
   }
   double penalty() {
     const long long n = (long long)design.size();

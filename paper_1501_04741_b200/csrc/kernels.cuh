@@ -908,6 +908,36 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 
 }  // namespace detail
 
+// Take a design-box node's uploaded value: poll its entry of the upload
+// buffer until the copy engine has replaced the sentinel, then re-arm it.
+// Relaxed loads (L2, no fence, no block barrier: the node's gather stays in
+// flight); the sweep runs in z order behind the upload, so the first load
+// almost always passes. Bounded (0.5 s of wall time): a value that never lands
+// is reported (LBGPU_E_NUMERIC at the call), never a hang.
+__device__ __forceinline__ double gate_take(const Gate& gt, long long o) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(gt.wd + o);
+  auto load = [p] {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+  };
+  unsigned long long v = load();
+  if (v == kGateEmpty) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((v = load()) == kGateEmpty) {
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 500000000ull) {
+        atomicExch(gt.err, 1u);
+        break;
+      }
+    }
+  }
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kGateEmpty) : "memory");
+  return __longlong_as_double((long long)v);
+}
+
 // ====================================================================
 // Sweep kernels. One thread per node, x fastest: grid (ceil(owned/BX), ny, nz).
 
@@ -922,7 +952,10 @@ __device__ __forceinline__ bool adjoint_node_full(const Launch& a, long long idx
 // against the f gathered here -- the base that iteration's adjoint used --
 // then the composite ascent step), exactly k_gradient<UPDATE>'s arithmetic,
 // so the primal collides with the new w it has just written.
-template <class L, class R, int CK, bool RESID, int FM = FM_DB, bool UPD = false>
+// GATED (lbgpu_primal_step_with_design, box-shaped design): a design-box
+// node's w is the just-uploaded value (gate_take, once its gather is in
+// flight), written to a.gate.w_out == a.t.w, which primal_node reads back.
+template <class L, class R, int CK, bool RESID, int FM = FM_DB, bool UPD = false, bool GATED = false>
 __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* dst, int x, int y,
                                             int z, unsigned long long& rmax) {
   using namespace detail;
@@ -954,6 +987,15 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* ds
     }
   } else if constexpr (FM == FM_DB) {
     gather<L, R, -1>(src, g.N, nb, f);
+    if constexpr (GATED) {
+      const Gate& gt = a.gate;
+      if (x >= gt.bx0 && x < gt.bx1 && y >= gt.by0 && y < gt.by1 && z >= gt.bz0 && z < gt.bz1) {
+        const long long o = (long long)(x - gt.bx0) +
+                            (long long)(gt.bx1 - gt.bx0) *
+                                ((y - gt.by0) + (long long)(gt.by1 - gt.by0) * (z - gt.bz0));
+        gt.w_out[idx] = gate_take(gt, o);
+      }
+    }
   } else {
     gather_m<L, R, -1, FM>(src, g.N, idx, nb, f);
   }
@@ -970,13 +1012,13 @@ __device__ __forceinline__ void primal_body(const Launch& a, const R* src, R* ds
 // Plain bounds: ptxas picks 64 regs (FP32) / 96-122 (FP64), no spills. Forcing
 // more blocks spills (FP32 C3 primal GB/s: 64 regs 5748, 48 regs 5480, 40
 // regs 4036); (128, 1) lets it take 106 regs (4827).
-template <class L, class R, int CK, bool RESID, bool UPD = false>
+template <class L, class R, int CK, bool RESID, bool UPD = false, bool GATED = false>
 __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ src,
                                                 R* __restrict__ dst) {
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (x < a.g.x1)
-    primal_body<L, R, CK, RESID, FM_DB, UPD>(a, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
+    primal_body<L, R, CK, RESID, FM_DB, UPD, GATED>(a, src, dst, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
@@ -1335,36 +1377,6 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
 #endif
 template <class R>
 constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
-
-// Take a design-box node's uploaded value: poll its entry of the upload
-// buffer until the copy engine has replaced the sentinel, then re-arm it.
-// Relaxed loads (L2, no fence, no block barrier: the node's gather stays in
-// flight); the sweep runs in z order behind the upload, so the first load
-// almost always passes. Bounded (0.5 s of wall time): a value that never lands
-// is reported (LBGPU_E_NUMERIC at the call), never a hang.
-__device__ __forceinline__ double gate_take(const Gate& gt, long long o) {
-  unsigned long long* p = reinterpret_cast<unsigned long long*>(gt.wd + o);
-  auto load = [p] {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-  };
-  unsigned long long v = load();
-  if (v == kGateEmpty) {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while ((v = load()) == kGateEmpty) {
-      __nanosleep(256);
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 500000000ull) {
-        atomicExch(gt.err, 1u);
-        break;
-      }
-    }
-  }
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kGateEmpty) : "memory");
-  return __longlong_as_double((long long)v);
-}
 
 // Fused primal + adjoint pair (product build): adjoint sweep n (base
 // f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
@@ -1960,6 +1972,12 @@ void primal_t(const SweepArgs& s, const void* src, void* dst) {
     if (s.upd) {
       k_primal<L, R, CK, false, true><<<grid, bx, 0, a.stream>>>(a, in, out);
       return;
+    }
+    if constexpr (L::DIM == 3) {
+      if (a.gate.wd) {  // upload-gated primal_step_with_design
+        k_primal<L, R, CK, false, false, true><<<grid, bx, 0, a.stream>>>(a, in, out);
+        return;
+      }
     }
   }
 #endif

@@ -296,23 +296,26 @@ def test_design_values_round_trip(lbgpu, oracle_mod, has_gpu):
 
 
 @pytest.mark.parametrize("nz", [8, 37])
-def test_primal_step_with_design_equals_upload_then_step(lbgpu, has_gpu, nz):
-    """lbgpu_primal_step_with_design (upload pipelined under the first sweep in
-    z-chunks; nz = 37 gives uneven chunks, nz = 8 takes the fallback) is
-    bitwise set_design_values + primal_step: states, residual, w."""
-    txt = case_text("mix3d", {"lattice.nz": nz})
-    for exact in (False, True):
+@pytest.mark.parametrize("prec", [64, 32])
+def test_primal_step_with_design_equals_upload_then_step(lbgpu, has_gpu, nz, prec):
+    """lbgpu_primal_step_with_design is bitwise set_design_values +
+    primal_step (states, residual, w) on each of its paths: one upload-gated
+    launch (box-shaped design, no residual on the first sweep), the z-chunked
+    upload (residual of a single sweep; nz = 37 gives uneven chunks), and the
+    fallback (nz = 8, the exact build)."""
+    txt = case_text("mix3d", {"lattice.nz": nz, "model.precision": prec})
+    for exact in (False, True) if prec == 64 else (False,):  # the bit-exact build is FP64
         a = lbgpu.Engine.from_config(txt, exact=exact)
         b = lbgpu.Engine.from_config(txt, exact=exact)
         for e in (a, b):
             e.init_state()
             e.primal_step(20)
         rng = np.random.default_rng(nz)
-        for k in (1, 3):
+        for k, resid in ((1, True), (3, True), (1, False), (2, False), (1, True)):
             vals = rng.uniform(0, 1, a.n_design)
-            ra = a.primal_step_with_design(vals, k)
+            ra = a.primal_step_with_design(vals, k, residual=resid)
             b.set_design_values(vals)
-            rb = b.primal_step(k)
+            rb = b.primal_step(k, residual=resid)
             assert ra == rb
             assert np.array_equal(a.get_state(0), b.get_state(0))
             assert np.array_equal(a.design_values(), vals)
