@@ -92,7 +92,7 @@ def main():
         import torch
         e = _engine()
         w = torch.from_numpy(e.design_values()).pin_memory().numpy()
-        for obj in (True, False, True):  # J read back, or not
+        for obj in (True, False, True, False, True, False):  # J read back, or not
             for _ in range(40):
                 e.pair_step_with_design(w, residual=False, objective=obj)
             e.finish()
@@ -104,6 +104,23 @@ def main():
             dt = (time.perf_counter() - t0) / K
             print(json.dumps({"objective": obj, "e2e_ms_per_step": dt * 1e3,
                               "e2e_mlups": e.n / dt / 1e6}), flush=True)
+    elif cmd == "e2e_alt":  # calls alternating with / without J, each timed (drift cancels)
+        import time
+        import torch
+        e = _engine()
+        w = torch.from_numpy(e.design_values()).pin_memory().numpy()
+        for _ in range(40):
+            e.pair_step_with_design(w, residual=False)
+        t = {True: [], False: []}
+        for k in range(600):
+            obj = k % 2 == 0
+            t0 = time.perf_counter()
+            e.pair_step_with_design(w, residual=False, objective=obj)
+            t[obj].append(time.perf_counter() - t0)
+        e.finish()
+        import statistics as S
+        print(json.dumps({"with_J_us": S.median(t[True]) * 1e6, "without_J_us": S.median(t[False]) * 1e6}),
+              flush=True)
     elif cmd == "l2gran":  # cudaLimitMaxL2FetchGranularity vs the objective / pair / e2e
         import ctypes
         import time
