@@ -467,7 +467,7 @@ struct lbgpu_engine {
     cudaFree(d_code), cudaFree(d_w), cudaFree(d_bcT), cudaFree(d_p0), cudaFree(d_p1);
     cudaFree(d_A), cudaFree(d_At), cudaFree(d_design), cudaFree(d_support), cudaFree(d_inlets);
     cudaFree(d_adj_side), cudaFree(d_grad_side), cudaFree(d_wvals), cudaFree(d_w2);
-    cudaFree(d_wgate);
+    cudaFree(d_wgate), cudaFree(d_inbox);
     cudaFree(d_terms), cudaFree(d_grad), cudaFree(d_scalar), cudaFree(d_ref), cudaFree(d_flags);
     cudaFree(d_ring);
     if (h_flags) cudaFreeHost(h_flags);
@@ -1270,8 +1270,26 @@ struct lbgpu_engine {
     CU(cudaMemcpyAsync(d_wgate, wd, sizeof(double) * n, cudaMemcpyHostToDevice, st_h2d));
     gate_armed = false;  // until the sweep is known to have re-armed every entry
   }
-  void gated_pair(const double* wd) {
+  // Support plane of J for the inbox (Gate::inbox): every support node in one
+  // column x = obj_plane_x with 1 <= x <= nx - 2 (config-built objectives:
+  // the plane nx - 1 - plane_offset), else -1.
+  int obj_plane_x = -2;  // -2: not determined yet
+  double* d_inbox = nullptr;
+  int obj_plane() {
+    if (obj_plane_x != -2) return obj_plane_x;
+    obj_plane_x = -1;
+    if (support.empty() || ghosts || dim != 3) return -1;
+    const int x0_ = int(support[0] % nx);
+    for (long long i : support)
+      if (int(i % nx) != x0_) return -1;
+    if (x0_ < 1 || x0_ > nx - 2) return -1;
+    CU(cudaMalloc(&d_inbox, sizeof(double) * m * (size_t)ny * nz));
+    obj_plane_x = x0_;
+    return obj_plane_x;
+  }
+  bool gated_pair(const double* wd, bool want_j) {
     gate_upload(wd);
+    const int ox = want_j ? obj_plane() : -1;
     NodeTables tn = T;
     tn.w = d_w2;     // the new design's full-grid buffer (design nodes written by the sweep)
     tn.w_adj = d_w;  // the previous design (the deferred adjoint half)
@@ -1280,10 +1298,12 @@ struct lbgpu_engine {
     sa.a.gate = gate_box;
     sa.a.gate.wd = d_wgate, sa.a.gate.w_out = d_w2;
     sa.a.gate.err = reinterpret_cast<unsigned*>(d_flags + 5);  // cleared by reset_flags
+    sa.a.gate.obj_x = ox, sa.a.gate.inbox = d_inbox;
     sa.dualw = true;
     fast::pair(sa, f[fc], f[1 - fc], v[vc], v[1 - vc]);
     launches += 1 + (sa.n_adj_side > 0);
     if (trace_on()) trace("K", st);
+    return ox >= 0;
   }
   void flush_pending() {
     if (!adj_pending) return;
@@ -1313,9 +1333,9 @@ struct lbgpu_engine {
     ++primal_steps;
     if (fuse) ++adjoint_steps;
     const bool gated = fuse && gate_ready();
-    bool published = false;
+    bool published = false, inbox = false;
     if (gated) {
-      gated_pair(wd);
+      inbox = gated_pair(wd, J != nullptr);
     } else {
       queue_design_upload(wd, ib, zb, true, true);
     }
@@ -1350,8 +1370,12 @@ struct lbgpu_engine {
     T.w = T.w_adj = d_w;
     w_host_stale = true;
     if (J) {
-      fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support,
-                            (long long)support.size(), d_terms, 0);
+      if (inbox)  // the fused sweep left the plane's populations in the inbox
+        fast::objective_inbox(launch(primal_steps - kb_p), dim, prec, d_inbox, d_support,
+                              (long long)support.size(), d_terms);
+      else
+        fast::objective_terms(launch(primal_steps - kb_p), dim, prec, f[fc], d_support,
+                              (long long)support.size(), d_terms, 0);
       ++launches;
       published = pairwise_queue(tree_support, d_terms, reinterpret_cast<double*>(d_flags + 4), true);
       if (trace_on()) trace("J", st);

@@ -1378,6 +1378,28 @@ __global__ void __launch_bounds__(128) k_adjoint_side(Launch a, const R* __restr
 template <class R>
 constexpr int kPairThreads = LBGPU_PAIR_BX * LBGPU_PAIR_BY;
 
+// The post values of node (x, y, z) that stream into the support plane x =
+// obj_x, stored at the receiving node's slot of the inbox (Gate): the pull
+// of node d reads post_P(d - e_P) with periodic wrap, so node s feeds d = s +
+// e_P. k_objective_inbox then reads the plane's populations coalesced instead
+// of 26 scattered lines per node.
+template <class L, class R>
+__device__ __forceinline__ void inbox_store(const Gate& gt, const Geom& g, int x, int y, int z,
+                                            const R* out) {
+  const int dx = gt.obj_x - x;
+  if (dx < -1 || dx > 1) return;
+  const long long S = (long long)g.ny * g.nz;
+  LBGPU_FOR(P, 0, L::M, {
+    constexpr int ex = cvel<L>(P, 0), ey = cvel<L>(P, 1), ez = cvel<L>(P, 2);
+    if (ex == dx) {
+      int yd = y + ey, zd = z + ez;
+      yd = yd < 0 ? g.ny - 1 : (yd >= g.ny ? 0 : yd);
+      zd = zd < 0 ? g.nz - 1 : (zd >= g.nz ? 0 : zd);
+      gt.inbox[P * S + yd + (long long)g.ny * zd] = double(out[P]);
+    }
+  });
+}
+
 // Fused primal + adjoint pair (product build): adjoint sweep n (base
 // f^{n+1}) and primal sweep n+1 read the same gathered f^{n+1}, so one kernel
 // gathers it once, takes its moments once (node_sums) and the node's
@@ -1476,6 +1498,9 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
     if constexpr (FM == FM_DB) {
       store_node<L, R, RESID>(fsrc, fdst, N, idx, f, out, rP, !face);
       push_halo<L, R, -1>(a, x, y, z, out);
+      if constexpr (GATED) {
+        if (a.gate.obj_x >= 0) inbox_store<L, R>(a.gate, g, x, y, z, out);
+      }
     } else {
       store_aa<L, R, -1, FM>(fdst, N, idx, nb, out);
     }
@@ -1766,6 +1791,29 @@ __global__ void k_objective_terms(Launch a, const R* __restrict__ p,
   const Nbr nb = make_nbr(g, x, y, z);
   R f[L::M];
   gather_m<L, R, -1, BM>(p, g.N, idx, nb, f);
+  R t;
+  if (!node_term<L, R>(a.M, f, t)) {
+    atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
+    t = R(NAN);
+  }
+  terms[i] = double(t);
+}
+
+// Objective terms from the inbox the gated fused sweep filled (Gate::inbox):
+// the same populations k_objective_terms gathers, read coalesced.
+template <class L, class R>
+__global__ void k_objective_inbox(Launch a, const double* __restrict__ inbox,
+                                  const long long* __restrict__ nodes, long long n,
+                                  double* __restrict__ terms) {
+  using namespace detail;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Geom& g = a.g;
+  const long long idx = nodes[i];
+  const int x = int(idx % g.nx), y = int((idx / g.nx) % g.ny), z = int(idx / ((long long)g.nx * g.ny));
+  const long long S = (long long)g.ny * g.nz, o = y + (long long)g.ny * z;
+  R f[L::M];
+  LBGPU_FOR(P, 0, L::M, { f[P] = R(inbox[P * S + o]); });
   R t;
   if (!node_term<L, R>(a.M, f, t)) {
     atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
@@ -2304,6 +2352,12 @@ void objective_terms(const Launch& a, int dim, int prec, const void* p, const lo
   const unsigned nb = unsigned((n + 127) / 128);
   LBGPU_LR_DISPATCH(dim, prec, LBGPU_FM_DISPATCH(bm, BM, (k_objective_terms<L, R, BM><<<nb, 128, 0, a.stream>>>(
                                     a, static_cast<const R*>(p), nodes, n, terms))));
+}
+void objective_inbox(const Launch& a, int dim, int prec, const double* inbox, const long long* nodes,
+                     long long n, double* terms) {
+  if (n <= 0) return;
+  const unsigned nb = unsigned((n + 127) / 128);
+  LBGPU_LR_DISPATCH(dim, prec, (k_objective_inbox<L, R><<<nb, 128, 0, a.stream>>>(a, inbox, nodes, n, terms)));
 }
 void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,
                  const long long* nodes, long long n, double* terms, int bm, int vm) {

@@ -61,6 +61,11 @@ struct Gate {
   double* w_out = nullptr;
   unsigned* err = nullptr;  // set when a value never landed (bounded wait)
   int bx0 = 0, bx1 = 0, by0 = 0, by1 = 0, bz0 = 0, bz1 = 0;
+  // J's inputs on the way (obj_x >= 0): the nodes of columns obj_x - 1 .. obj_x + 1
+  // also store the post values that stream into the objective's support plane
+  // x = obj_x, at inbox[P (ny nz) + y + ny z] of the receiving node (y, z)
+  double* inbox = nullptr;
+  int obj_x = -1;
 };
 
 // One-shot design update carried by the next primal sweep (k_primal UPD):
@@ -109,6 +114,8 @@ struct SweepArgs {
                 double* w_rw, double zeta, double lambda, int accumulate, int bm, int vm); \
   void objective_terms(const Launch& a, int dim, int prec, const void* p,                  \
                        const long long* nodes, long long n, double* terms, int bm);        \
+  void objective_inbox(const Launch& a, int dim, int prec, const double* inbox,            \
+                       const long long* nodes, long long n, double* terms);                \
   void inlet_terms(const Launch& a, int dim, int prec, const void* p, const void* q,       \
                    const long long* nodes, long long n, double* terms, int bm, int vm);    \
   void layout(const Geom& g, int dim, int prec, int field, bool to_ref, const void* in,    \
