@@ -1958,6 +1958,13 @@ struct lbgpu_engine {
     launches += 2 + tr.top;
     return false;
   }
+  // the objective's terms of a double-buffered state into d_terms (no sync)
+  void objective_terms_queue(const void* P) {
+    const Launch a = launch(primal_steps - kb_p);
+    if (exact) exact::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, 0);
+    else fast::objective_terms(a, dim, prec, P, d_support, (long long)support.size(), d_terms, 0);
+    ++launches;
+  }
   double objective(const void* buf = nullptr) {
     const Launch a = launch(primal_steps - kb_p);
     const void* P = buf ? buf : f[fc];
@@ -2077,7 +2084,8 @@ struct lbgpu_engine {
     void* work;   // ping-pong partners for forward segments
     void* work2;
     const Schedule* sch;
-    double gdp = 0.0;
+    double* d_gs = nullptr;  // per back step: the inlet_dp term's tree sum (summed on the host
+    long long gn = 0;        // at the end, in step order: no host sync per step)
     // k >= 1 sweeps from `from`, the last one landing in `to` (via `tmp`)
     void fwd(const void* from, void* to, long long k, void* tmp) {
       const void* src = from;
@@ -2096,7 +2104,7 @@ struct lbgpu_engine {
       if (!e->inlets.empty()) {
         if (e->exact) exact::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
         else fast::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
-        gdp += e->pairwise(e->tree_inlet, e->d_terms);
+        e->pairwise_queue(e->tree_inlet, e->d_terms, d_gs + gn++);
       }
       e->M.obj_on = sum ? 1 : 0;
       e->adjoint_raw(0, base, e->v[e->vc], e->v[1 - e->vc], false, nullptr, true);
@@ -2147,8 +2155,11 @@ struct lbgpu_engine {
     if (N < 1) throw Fail{LBGPU_E_ARG, "unsteady adjoint needs at least one step"};
     const long long nslots = std::max<long long>(1, std::min<long long>(max_slots, N));
     std::vector<void*> slots;
+    double* d_js = nullptr;  // J of each summed step, and the inlet_dp sums of the back steps
+    double* d_gs = nullptr;
     auto release = [&] {
       for (void* p : slots) cudaFree(p);
+      cudaFree(d_js), cudaFree(d_gs);
     };
     try {
       for (long long i = 0; i < nslots + 2; ++i) {
@@ -2168,11 +2179,13 @@ struct lbgpu_engine {
       const long long steps0 = primal_steps;
       reset_flags();
       CU(cudaMemcpyAsync(s0, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
-      Unsteady U{this, sum_obj, {}, slots[0], slots[1], &sch};
+      CU(cudaMalloc(&d_js, sizeof(double) * (N + 1)));
+      CU(cudaMalloc(&d_gs, sizeof(double) * (N + 1)));
+      Unsteady U{this, sum_obj, {}, slots[0], slots[1], &sch, d_gs, 0};
       for (long long i = 2; i < (long long)slots.size(); ++i) U.free_slots.push_back(slots[i]);
       // first pass: states 1..N and the objective, placing the schedule's
       // checkpoints (chain) and, in its last segment, every inner state
-      double Jv = 0.0;
+      long long jn = 0;
       std::vector<std::pair<long long, void*>> chain{{0, s0}};
       std::vector<void*> tail;  // the last segment's stored inner states
       long long a = 0;
@@ -2180,7 +2193,10 @@ struct lbgpu_engine {
       auto step_to = [&](long long n, void* dst) {
         primal_raw(src, dst, false, nullptr, true);
         src = dst;
-        if (sum_obj || n == N) Jv += objective(dst);
+        if (sum_obj || n == N) {  // J of state n, queued (summed on the host at the end)
+          objective_terms_queue(dst);
+          pairwise_queue(tree_support, d_terms, d_js + jn++);
+        }
       };
       for (;;) {
         const long long n = N - a;
@@ -2234,9 +2250,15 @@ struct lbgpu_engine {
       // f^N stays in f[fc] (sN); f[1 - fc] (s0) is scratch again
       if (g && !design.empty())
         CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * design.size(), cudaMemcpyDeviceToHost, st));
+      std::vector<double> js(static_cast<size_t>(jn)), gs(static_cast<size_t>(U.gn));
+      if (jn) CU(cudaMemcpyAsync(js.data(), d_js, sizeof(double) * jn, cudaMemcpyDeviceToHost, st));
+      if (U.gn) CU(cudaMemcpyAsync(gs.data(), d_gs, sizeof(double) * U.gn, cudaMemcpyDeviceToHost, st));
       sync();
       check_bad("unsteady iteration");
-      if (gdp) *gdp = U.gdp;
+      double Jv = 0.0, gd = 0.0;  // the per-step sums in the order the steps ran
+      for (double x : js) Jv += x;
+      for (double x : gs) gd += x;
+      if (gdp) *gdp = gd;
       if (J) *J = Jv;
       if (fsteps) *fsteps = primal_steps - steps0;
     } catch (...) {
