@@ -1399,11 +1399,13 @@ struct lbgpu_engine {
 
   // New design values (DesignField::nodes order, host memory) followed by n
   // primal sweeps: optimizer.cpp:200-202 (the MMA update's write-back, then
-  // solve_fixed_point). The first sweep runs in z-chunks, each waiting only
-  // for its own slice of the upload, so the H2D copy overlaps the sweep
-  // (design nodes ascend in flat index, i.e. z-major, and a sweep node
-  // reads w only at itself). Falls back to upload-then-sweep where chunking
-  // does not apply (exact build: host pow tables; 2D; NCCL halo overlap).
+  // solve_fixed_point). The H2D copy overlaps the first sweep: for a
+  // box-shaped design, ONE gated launch (each design node's thread waits for
+  // its own value, gate_upload); otherwise z-chunks, each waiting only for
+  // its own slice of the upload (design nodes ascend in flat index, i.e.
+  // z-major, and a sweep node reads w only at itself). Falls back to
+  // upload-then-sweep where neither applies (exact build: host pow tables;
+  // 2D; NCCL halo overlap).
   static constexpr int kChunks = 8;
   double design_steps(const double* wd, long long nsteps, bool want_resid) {
     require_solo();
