@@ -214,7 +214,9 @@ def run_reference(args, rank: int, world: int) -> None:
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": (tp + ta) / steps * 1e3, "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "sample_nodes": nodes},
+        "config": {"workload": wl["desc"], "id": wl["id"], "sample_nodes": nodes,
+                   "path": "the reference's PartitionedRun (oracle/_ref, built from its sources)",
+                   "parallelism": f"host CPU, {cores} threads"},
         "primal_mlups": nodes * steps / tp / 1e6, "adjoint_mlups": nodes * steps / ta / 1e6,
         "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": cores, "cpu": cpu_model(),
                          "kind": "reference", "sample": sample},
