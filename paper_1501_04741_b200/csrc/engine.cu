@@ -335,6 +335,12 @@ __global__ void k_fill_bits(unsigned long long* p, long long n, unsigned long lo
   if (i < n) p[i] = v;
 }
 
+__global__ void k_gather_design(const double* __restrict__ full, const long long* __restrict__ nodes,
+                                long long n, double* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = full[nodes[i]];
+}
+
 __global__ void k_scatter_design(const double* __restrict__ vals, const long long* __restrict__ nodes,
                                  long long n, double* __restrict__ w) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -855,12 +861,16 @@ struct lbgpu_engine {
     else go(s);
   }
   // One adjoint sweep src -> dst against the primal pull buffer `base`.
+  // adj_gacc: the next gathering FP64 sweeps also accumulate the design
+  // gradient of their inputs there (k_adjoint GRAD; the unsteady back step)
+  double* adj_gacc = nullptr;
   void adjoint_raw(int kernel, const void* base, const void* src, void* dst, bool resid,
                    unsigned long long* slot, bool exch) {
     ++adjoint_steps;
     ++launches;
     SweepArgs s = sweep(adjoint_steps - kb_a, resid, slot);
-    if (kernel == 0 && mom_base && mom_base == base) s.mom = d_mom;
+    if (kernel == 0 && mom_base && mom_base == base && !adj_gacc) s.mom = d_mom;
+    s.a.upd.gacc = adj_gacc;
     if (aa) {
       if (resid) require_db("a step residual");
       if (kernel != 0) require_db("the dual-sweep adjoint kernel");
@@ -2088,6 +2098,7 @@ struct lbgpu_engine {
     const Schedule* sch;
     double* d_gs = nullptr;  // per back step: the inlet_dp term's tree sum (summed on the host
     long long gn = 0;        // at the end, in step order: no host sync per step)
+    double* d_gacc = nullptr;  // fused: per-node gradient sums, accumulated by the adjoint sweep
     // k >= 1 sweeps from `from`, the last one landing in `to` (via `tmp`)
     void fwd(const void* from, void* to, long long k, void* tmp) {
       const void* src = from;
@@ -2101,15 +2112,19 @@ struct lbgpu_engine {
     void back_step(const void* base) {
       const long long nd = (long long)e->design.size();
       const Launch a = e->launch(e->adjoint_steps - e->kb_a);
-      if (e->exact) exact::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
-      else fast::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
+      if (!d_gacc) {  // else the adjoint sweep below adds each design node's term
+        if (e->exact) exact::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
+        else fast::gradient(a, e->dim, e->prec, 0, false, base, e->v[e->vc], e->d_design, nd, e->d_grad, nullptr, 0, 0, 1, 0, 0);
+      }
       if (!e->inlets.empty()) {
         if (e->exact) exact::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
         else fast::inlet_terms(a, e->dim, e->prec, base, e->v[e->vc], e->d_inlets, (long long)e->inlets.size(), e->d_terms, 0, 0);
         e->pairwise_queue(e->tree_inlet, e->d_terms, d_gs + gn++);
       }
       e->M.obj_on = sum ? 1 : 0;
+      e->adj_gacc = d_gacc;
       e->adjoint_raw(0, base, e->v[e->vc], e->v[1 - e->vc], false, nullptr, true);
+      e->adj_gacc = nullptr;
       e->vc ^= 1;
       e->M.obj_on = 1;
     }
@@ -2159,10 +2174,15 @@ struct lbgpu_engine {
     std::vector<void*> slots;
     double* d_js = nullptr;  // J of each summed step, and the inlet_dp sums of the back steps
     double* d_gs = nullptr;
+    double* d_gacc = nullptr;  // per-node gradient sums when the adjoint sweep carries them
     auto release = [&] {
       for (void* p : slots) cudaFree(p);
-      cudaFree(d_js), cudaFree(d_gs);
+      cudaFree(d_js), cudaFree(d_gs), cudaFree(d_gacc);
     };
+    // The back step's gradient rides in its adjoint sweep (k_adjoint GRAD)
+    // where that sweep gathers an FP64 double-buffered base and every design
+    // node is interior; bitwise the separate k_gradient pass.
+    const bool fuse_grad = !exact && prec == 64 && xmode == 0 && grad_side.empty() && !design.empty();
     try {
       for (long long i = 0; i < nslots + 2; ++i) {
         void* p = nullptr;
@@ -2183,7 +2203,11 @@ struct lbgpu_engine {
       CU(cudaMemcpyAsync(s0, f[fc], field_bytes(), cudaMemcpyDeviceToDevice, st));
       CU(cudaMalloc(&d_js, sizeof(double) * (N + 1)));
       CU(cudaMalloc(&d_gs, sizeof(double) * (N + 1)));
-      Unsteady U{this, sum_obj, {}, slots[0], slots[1], &sch, d_gs, 0};
+      if (fuse_grad) {
+        CU(cudaMalloc(&d_gacc, sizeof(double) * this->N));  // this->N: nodes (N here counts steps)
+        CU(cudaMemsetAsync(d_gacc, 0, sizeof(double) * this->N, st));
+      }
+      Unsteady U{this, sum_obj, {}, slots[0], slots[1], &sch, d_gs, 0, d_gacc};
       for (long long i = 2; i < (long long)slots.size(); ++i) U.free_slots.push_back(slots[i]);
       // first pass: states 1..N and the objective, placing the schedule's
       // checkpoints (chain) and, in its last segment, every inner state
@@ -2250,6 +2274,11 @@ struct lbgpu_engine {
         U.reverse(chain[j].first, chain[j + 1].first, chain[j].second);
       }
       // f^N stays in f[fc] (sN); f[1 - fc] (s0) is scratch again
+      if (d_gacc) {
+        const long long nd = (long long)design.size();
+        k_gather_design<<<unsigned((nd + 255) / 256), 256, 0, st>>>(d_gacc, d_design, nd, d_grad);
+        ++launches;
+      }
       if (g && !design.empty())
         CU(cudaMemcpyAsync(g, d_grad, sizeof(double) * design.size(), cudaMemcpyDeviceToHost, st));
       std::vector<double> js(static_cast<size_t>(jn)), gs(static_cast<size_t>(U.gn));

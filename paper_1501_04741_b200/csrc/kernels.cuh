@@ -1081,8 +1081,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : L
 // the rare side-list nodes (synthetic-objective support, support nodes on a
 // face) to k_adjoint_side.
 // BM / VM: addressing modes of the base f and of v (in-place v: src == dst).
+// GRAD (FP64 split sweep of a double-buffered field): at an interior design
+// node, also k_gradient's term of this sweep's own inputs -- the base f in
+// registers, v staged in shared memory, the same design_gradient call -- added
+// to a.upd.gacc[node]: the unsteady adjoint's back step then needs no
+// separate gradient pass over the design nodes.
 template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM, int BM = FM_DB,
-          int VM = FM_DB>
+          int VM = FM_DB, bool GRAD = false>
 __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restrict__ base,
                                              const R* src, R* dst, const R* __restrict__ mom,
                                              int x, int y, int z, unsigned long long& rmax) {
@@ -1151,6 +1156,17 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         flow_sums<L, R>(fin, rho, jv);
 #pragma unroll
         for (int k = 0; k < L::MT; ++k) T += fin[L::MF + k];
+        if constexpr (GRAD && kStage) {
+          if ((code & (TAG_MASK | CODE_AXIS_BITS)) == (TAG_INTERIOR | CODE_DESIGN_INT)) {
+            cp_async_wait_all();
+            const double w = a.t.w[idx];
+            const PowPair pp = node_pp<false>(a.M, a.t, idx, code | CODE_HAS_W, w);
+            double gv = 0.0;
+            if (!design_gradient<L, R, 128>(a.M, pp, fin, fin + L::MF, R(w), my, my + L::MF * 128, gv))
+              ok = false;
+            a.upd.gacc[idx] = a.upd.gacc[idx] + gv;
+          }
+        }
       }
       if constexpr (kStage) {
         cp_async_wait_all();
@@ -1263,7 +1279,7 @@ __global__ void __launch_bounds__(128) k_base_moments(Launch a, const R* __restr
                          : (MOM) ? (sizeof(R) == 4 ? LBGPU_ADJ_MINB32_MOM : LBGPU_ADJ_MINB_MOM) \
                                  : (sizeof(R) == 4 ? LBGPU_ADJ_MINB32 : LBGPU_ADJ_MINB))
 
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
+template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM, bool GRAD = false>
 __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
                                                                 const R* __restrict__ base,
                                                                 const R* __restrict__ src,
@@ -1272,8 +1288,8 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
   const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rmax = 0;
   if (x < a.g.x1)
-    adjoint_body<L, R, CK, AK, RESID, SPLIT, MOM>(a, base, src, dst, mom, x, blockIdx.y,
-                                                  a.g.z0 + blockIdx.z, rmax);
+    adjoint_body<L, R, CK, AK, RESID, SPLIT, MOM, FM_DB, FM_DB, GRAD>(a, base, src, dst, mom, x, blockIdx.y,
+                                                                      a.g.z0 + blockIdx.z, rmax);
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
@@ -2051,6 +2067,12 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
         int nzs = a.g.nz;
         if (s.z1 > s.z0) a.g.z0 = s.z0, nzs = s.z1 - s.z0;  // z-chunk (design pair)
         dim3 grid((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, nzs);
+        if constexpr (split && !MOM && !RES && sizeof(R) == 8) {
+          if (a.upd.gacc) {  // the sweep also accumulates the design gradient
+            k_adjoint<L, R, CK, AK, false, true, false, true><<<grid, bx, 0, a.stream>>>(a, b, in, out, mom);
+            return;
+          }
+        }
         k_adjoint<L, R, CK, AK, RES, split, MOM><<<grid, bx, 0, a.stream>>>(a, b, in, out, mom);
       }
     }

@@ -76,6 +76,9 @@ struct Upd {
   const void* v = nullptr;  // adjoint state (double-buffered post layout)
   double* w = nullptr;      // design, updated in place
   double zeta = 0.0, lambda = 0.0;
+  // adjoint sweep (k_adjoint GRAD, the unsteady adjoint's back step): the
+  // design gradient of the sweep's own inputs (base f, v) accumulated per node
+  double* gacc = nullptr;
 };
 
 struct Launch {
