@@ -27,6 +27,8 @@ Workloads:
 
 --gpus N > 1 launches the N ranks itself (torch.distributed.run) unless it is
 already running under one; it fails when fewer than N GPUs are visible.
+LBGPU_BENCH_SLAB_RING=1 at N = 1 runs the N > 1 code path on one GPU (one slab
+over a single-rank NCCL ring): a check of that path, not a scaling number.
 
 Timing: W untimed step pairs, then exactly K timed pairs bracketed by a
 barrier and device synchronisation, CUDA events on the engine's stream, max
@@ -288,7 +290,18 @@ def main() -> None:
 
     wl = workload(args, world)
     txt = wl["txt"]
-    if world == 1:
+    # LBGPU_BENCH_SLAB_RING=1 at N = 1: the N > 1 code path on one GPU -- one
+    # slab in ghost layout over a single-rank NCCL ring (its own neighbour both
+    # ways), every halo exchange included. A check of the multi-GPU path where
+    # only one GPU is available; not a scaling number.
+    ring = world == 1 and os.environ.get("LBGPU_BENCH_SLAB_RING") == "1"
+    if ring:
+        eng = P.Engine.slab_from_config(txt, None, 1, -1, device=local, streaming=wl["streaming"])
+        eng.attach_nccl(P.nccl_unique_id(), 1, 0)
+        sl = eng.slab()
+        nodes = sl["span"] * eng.shape[1] * eng.shape[2]
+        wl["parallelism"] = "1 GPU, one slab over a single-rank NCCL ring (check of the N > 1 path)"
+    elif world == 1:
         eng = P.Engine.from_config(txt, device=local, streaming=wl["streaming"])
         nodes = eng.n
     else:
@@ -366,7 +379,7 @@ def main() -> None:
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath) and wl["id"] == "C3" and world == 1:
+    if os.path.exists(tpath) and wl["id"] == "C3" and world == 1 and not ring:
         with open(tpath) as fh:
             tj = json.load(fh)
         traffic = tj.get("pair_bytes_per_launch" if fused else "adjoint_bytes_per_launch")
@@ -375,7 +388,7 @@ def main() -> None:
     w_host = torch.from_numpy(eng.design_values()).pin_memory()
     w_np = w_host.numpy()
     eng.set_design_values(w_np)
-    if wl["streaming"] == "double" and world == 1:
+    if wl["streaming"] == "double" and world == 1 and not ring:
         # lbgpu_pair_step_with_design: the design vector (DesignField::nodes
         # order, 16 MB at C3) H2D from pinned memory, one primal sweep, one
         # adjoint sweep against the new state, J of the new state back to the
@@ -452,7 +465,7 @@ def main() -> None:
         return
 
     cpu = None
-    if world == 1 and wl["id"] == "C3" and not args.no_cpu_baseline:
+    if world == 1 and wl["id"] == "C3" and not args.no_cpu_baseline and not ring:
         try:
             cpu = cpu_baseline(txt, nodes)
         except Exception as exc:  # reported, never silently substituted

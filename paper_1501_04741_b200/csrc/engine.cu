@@ -2688,7 +2688,11 @@ int lbgpu_attach_nccl(lbgpu_engine* e, const void* uid, int nranks, int rank) {
     if (r != ncclSuccess) throw Fail{LBGPU_E_NUMERIC, std::string("NCCL: ") + nccl().GetErrorString(r)};
     e->rank = rank, e->nranks = nranks;
     e->xmode = 2;
-    CU(cudaStreamCreateWithFlags(&e->st_comm, cudaStreamNonBlocking));
+    // the halo's pack / NCCL / unpack kernels take precedence over the
+    // interior sweep's pending blocks, so the exchange never queues behind it
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&e->st_comm, cudaStreamNonBlocking, hi));
     CU(cudaEventCreateWithFlags(&e->ev_bnd, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&e->ev_halo, cudaEventDisableTiming));
   });

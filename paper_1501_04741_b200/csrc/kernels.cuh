@@ -2012,20 +2012,41 @@ __global__ void k_halo_runpack(Geom g, R* __restrict__ buf, const R* __restrict_
 // Host-side launchers (one set per build), dispatched by the engine.
 
 
-// part: 0 all owned columns, 1 interior columns only (x0+1 .. x1-2),
-// 2 the two boundary columns only (see SweepArgs).
+// part (SweepArgs): 0 all owned columns; 2 the boundary strips, kStrip
+// columns at each end of the slab (whole coalesced rows, computed first so
+// their halo can travel; a kernel over single boundary columns would read 26
+// scattered lines per node); 1 the columns between the strips.
+constexpr int kStrip = 32;
+inline int part_ranges(int part, int x0, int x1, int r[2][2]) {
+  const bool strips = x1 - x0 > 2 * kStrip;
+  if (part == 0 || (part == 2 && !strips)) {
+    r[0][0] = x0, r[0][1] = x1;
+    return 1;
+  }
+  if (part == 1) {
+    if (!strips) return 0;
+    r[0][0] = x0 + kStrip, r[0][1] = x1 - kStrip;
+    return 1;
+  }
+  r[0][0] = x0, r[0][1] = x0 + kStrip, r[1][0] = x1 - kStrip, r[1][1] = x1;
+  return 2;
+}
+// each x-range of s.part, as a Launch whose owned columns are that range
+template <class F>
+static void for_part(const SweepArgs& s, F&& fn) {
+  int r[2][2];
+  const int n = part_ranges(s.part, s.a.g.x0, s.a.g.x1, r);
+  for (int k = 0; k < n; ++k) {
+    Launch a = s.a;
+    a.g.x0 = r[k][0], a.g.x1 = r[k][1];
+    fn(a);
+  }
+}
+
 template <class L, class R, int CK, bool RES>
-void primal_t(const SweepArgs& s, const void* src, void* dst) {
+void primal_range(const SweepArgs& s, Launch a, const void* src, void* dst) {
   const R* in = static_cast<const R*>(src);
   R* out = static_cast<R*>(dst);
-  Launch a = s.a;
-  if (s.part == 2) {
-    const long long n = 2ll * a.g.ny * a.g.nz;
-    k_primal_cols<L, R, CK, RES><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
-        a, in, out, a.g.x0, a.g.x1 - 1);
-    return;
-  }
-  if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
   if (a.g.x1 <= a.g.x0) return;
   const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
   int nzs = a.g.nz;
@@ -2047,21 +2068,19 @@ void primal_t(const SweepArgs& s, const void* src, void* dst) {
 #endif
   k_primal<L, R, CK, RES><<<grid, bx, 0, a.stream>>>(a, in, out);
 }
+template <class L, class R, int CK, bool RES>
+void primal_t(const SweepArgs& s, const void* src, void* dst) {
+  for_part(s, [&](Launch a) { primal_range<L, R, CK, RES>(s, a, src, dst); });
+}
 template <class L, class R, int CK, int AK, bool RES>
 void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst) {
   const R* b = static_cast<const R*>(base);
   const R* in = static_cast<const R*>(src);
   R* out = static_cast<R*>(dst);
   constexpr bool split = !LBGPU_EXACT && AK == 0;
-  Launch a = s.a;
   const R* mom = static_cast<const R*>(s.mom);
   auto go = [&]<bool MOM>() {
-    if (s.part == 2) {
-      const long long n = 2ll * a.g.ny * a.g.nz;
-      k_adjoint_cols<L, R, CK, AK, RES, split, MOM><<<unsigned((n + 127) / 128), 128, 0, a.stream>>>(
-          a, b, in, out, mom, a.g.x0, a.g.x1 - 1);
-    } else {
-      if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+    for_part(s, [&](Launch a) {
       if (a.g.x1 > a.g.x0) {
         const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
         int nzs = a.g.nz;
@@ -2075,7 +2094,7 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
         }
         k_adjoint<L, R, CK, AK, RES, split, MOM><<<grid, bx, 0, a.stream>>>(a, b, in, out, mom);
       }
-    }
+    });
   };
   if constexpr (split) {
     if (mom) go.template operator()<true>();
@@ -2086,7 +2105,7 @@ void adjoint_t(const SweepArgs& s, const void* base, const void* src, void* dst)
   // side-list nodes go with the full sweep, or with the boundary part so that
   // they are final before a halo is packed
   if (split && s.n_adj_side > 0 && s.part != 1)
-    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
+    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, s.a.stream>>>(
         s.a, b, in, out, s.adj_side, s.n_adj_side);
 }
 
@@ -2159,14 +2178,8 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
   const R* vsrc = static_cast<const R*>(vs_);
   R* fdst = static_cast<R*>(fd_);
   R* vdst = static_cast<R*>(vd_);
-  Launch a = s.a;
   constexpr int TB = kPairThreads<R>;
-  if (s.part == 2) {
-    const long long n = 2ll * a.g.ny * a.g.nz;
-    k_pair_cols<L, R, CK, RES><<<unsigned((n + TB - 1) / TB), TB, 0, a.stream>>>(
-        a, fsrc, fdst, vsrc, vdst, a.g.x0, a.g.x1 - 1);
-  } else {
-    if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
+  for_part(s, [&](Launch a) {
     if (a.g.x1 > a.g.x0) {
       const int wx = a.g.x1 - a.g.x0;
       const int bx = wx >= LBGPU_PAIR_BX ? LBGPU_PAIR_BX : (wx >= 64 ? 64 : 32);
@@ -2186,12 +2199,12 @@ void pair_t(const SweepArgs& s, const void* fs_, void* fd_, const void* vs_, voi
       }
       if (!done) k_pair<L, R, CK, RES><<<grid, dim3(bx, by), 0, a.stream>>>(a, fsrc, fdst, vsrc, vdst);
     }
-  }
+  });
   if (s.n_adj_side > 0 && s.part != 1) {
     Launch as = s.a;
     if (s.dualw) as.t.w = as.t.w_adj;  // the side nodes' adjoint is the previous design's
     as.fl.resid = s.a.fl.aux;  // the side nodes' residual is the adjoint's
-    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, a.stream>>>(
+    k_adjoint_side<L, R, CK, RES><<<unsigned((s.n_adj_side + 127) / 128), 128, 0, as.stream>>>(
         as, fsrc, vsrc, vdst, s.adj_side, s.n_adj_side);
   }
 }
@@ -2220,16 +2233,11 @@ void base_moments(const Launch& a, int dim, int prec, int bm, const void* base, 
 // launch(a, grid, block, c0, c1): c0 >= 0 selects the boundary-column mode
 template <class F>
 static void aa_grid(const SweepArgs& s, F&& launch) {
-  Launch a = s.a;
-  if (s.part == 2) {
-    const long long n = 2ll * a.g.ny * a.g.nz;
-    launch(a, dim3(unsigned((n + 127) / 128)), dim3(128), a.g.x0, a.g.x1 - 1);
-    return;
-  }
-  if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
-  if (a.g.x1 <= a.g.x0) return;
-  const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-  launch(a, dim3((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz), dim3(bx), -1, -1);
+  for_part(s, [&](Launch a) {
+    if (a.g.x1 <= a.g.x0) return;
+    const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
+    launch(a, dim3((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz), dim3(bx), -1, -1);
+  });
 }
 void primal_aa(const SweepArgs& s, void* A) {
 #if !LBGPU_EXACT
@@ -2299,20 +2307,15 @@ void pair_aa(const SweepArgs& s, void* F, void* V) {
       else side.template operator()<FM_E, FM_E>();
     }
     auto go = [&]<int FM, int VM>() {
-      Launch a = s.a;
       constexpr int TB = kPairThreads<R>;
-      if (s.part == 2) {
-        const long long n = 2ll * a.g.ny * a.g.nz;
-        k_pair_aa<L, R, CKV, FM, VM><<<unsigned((n + TB - 1) / TB), TB, 0, a.stream>>>(a, f, v, a.g.x0, a.g.x1 - 1);
-        return;
-      }
-      if (s.part == 1) a.g.x0 += 1, a.g.x1 -= 1;
-      if (a.g.x1 <= a.g.x0) return;
-      const int wx = a.g.x1 - a.g.x0;
-      const int bx = wx >= LBGPU_AAPAIR_BX ? LBGPU_AAPAIR_BX : (wx >= 64 ? 64 : 32);
-      const int by = TB / bx;
-      dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, a.g.nz);
-      k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v, -1, -1);
+      for_part(s, [&](Launch a) {
+        if (a.g.x1 <= a.g.x0) return;
+        const int wx = a.g.x1 - a.g.x0;
+        const int bx = wx >= LBGPU_AAPAIR_BX ? LBGPU_AAPAIR_BX : (wx >= 64 ? 64 : 32);
+        const int by = TB / bx;
+        dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, a.g.nz);
+        k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v, -1, -1);
+      });
     };
     if (s.fm == FM_O && s.vm == FM_O) go.template operator()<FM_O, FM_O>();
     else if (s.fm == FM_O) go.template operator()<FM_O, FM_E>();
