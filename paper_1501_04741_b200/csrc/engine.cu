@@ -821,7 +821,7 @@ struct lbgpu_engine {
   }
 
   // ------------------------------------------------------------ sweeps
-  // NCCL mode: the two boundary columns first, their halo on the comm stream
+  // NCCL mode: the boundary strips first, their halo on the comm stream
   // while the interior columns compute, joined before the next sweep.
   // kind: the exchange after the sweep (0 double-buffered; in place: 1 forward
   // after a sweep from O, 2 reverse after a sweep from E; kernels.cuh)

@@ -1022,26 +1022,8 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
-// The two boundary columns (c0, c1) of a slab, one thread per (column, y, z):
-// computed first so their halo can travel while k_primal does the interior.
-template <class L, class R, int CK, bool RESID>
-__global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restrict__ src,
-                                                     R* __restrict__ dst, int c0, int c1) {
-  const long long yz = (long long)a.g.ny * a.g.nz;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long rmax = 0;
-  if (t < 2 * yz) {
-    const long long r = t % yz;
-    primal_body<L, R, CK, RESID>(a, src, dst, t < yz ? c0 : c1, int(r % a.g.ny),
-                                 int(r / a.g.ny), rmax);
-  }
-  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
-}
-
 // In-place primal sweep (AA streaming, fast build) from layout FM over the
-// owned columns of the 3-D grid, or, with c0 >= 0, over the slab's two
-// boundary columns c0, c1 only (one thread per (column, y, z); a runtime
-// switch, uniform per launch, to halve the instantiations).
+// owned columns of the 3-D grid.
 // Register bound of the in-place primal (FP64): left alone, the sweep from E
 // keeps its 26 scattered store addresses live across the collision (182
 // registers, 2 blocks/SM). Measured C3 primal GB/s at 1/2/3/4 blocks per SM:
@@ -1055,20 +1037,10 @@ __global__ void __launch_bounds__(128) k_primal_cols(Launch a, const R* __restri
 #endif
 template <class L, class R, int CK, int FM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : LBGPU_AA_PRIMAL_MINB32)
-    k_primal_aa(Launch a, R* A, int c0, int c1) {
+    k_primal_aa(Launch a, R* A) {
   unsigned long long rmax = 0;
-  if (c0 >= 0) {
-    const long long yz = (long long)a.g.ny * a.g.nz;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t < 2 * yz) {
-      const long long r = t % yz;
-      primal_body<L, R, CK, false, FM>(a, A, A, t < yz ? c0 : c1, int(r % a.g.ny),
-                                       int(r / a.g.ny), rmax);
-    }
-  } else {
-    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (x < a.g.x1) primal_body<L, R, CK, false, FM>(a, A, A, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
-  }
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < a.g.x1) primal_body<L, R, CK, false, FM>(a, A, A, x, blockIdx.y, a.g.z0 + blockIdx.z, rmax);
 }
 
 // Adjoint sweep (adjoint_step, adjoint.cpp:206-254, in pull form): gathers v
@@ -1293,26 +1265,8 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
   if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
 }
 
-template <class L, class R, int CK, int AK, bool RESID, bool SPLIT, bool MOM>
-__global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
-                                                                     const R* __restrict__ base,
-                                                                     const R* __restrict__ src,
-                                                                     R* __restrict__ dst,
-                                                                     const R* __restrict__ mom,
-                                                                     int c0, int c1) {
-  const long long yz = (long long)a.g.ny * a.g.nz;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long rmax = 0;
-  if (t < 2 * yz) {
-    const long long r = t % yz;
-    adjoint_body<L, R, CK, AK, RESID, SPLIT, MOM>(a, base, src, dst, mom, t < yz ? c0 : c1,
-                                                  int(r % a.g.ny), int(r / a.g.ny), rmax);
-  }
-  if constexpr (RESID) detail::block_max_bits(rmax, a.fl.resid);
-}
-
 // In-place adjoint sweep (AA streaming, fast build): base f read under BM, v
-// updated in place from layout VM; COLS as k_primal_aa.
+// updated in place from layout VM.
 // In-place adjoint (FP64), C3 GB/s at 2/3/4 blocks per SM: 4,947 / 5,988 /
 // 5,824 (4 spills 144-472 B in the sweeps from E).
 #ifndef LBGPU_AA_ADJ_MINB
@@ -1325,24 +1279,12 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint_cols(Launch a,
 template <class L, class R, int CK, int BM, int VM, bool MOM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_ADJ_MINB
                                                       : (MOM ? LBGPU_ADJ_MINB32_MOM : LBGPU_AA_ADJ_MINB32))
-    k_adjoint_aa(Launch a, const R* __restrict__ base,
-                                                            R* V, const R* __restrict__ mom,
-                                                            int c0, int c1) {
+    k_adjoint_aa(Launch a, const R* __restrict__ base, R* V, const R* __restrict__ mom) {
   unsigned long long rmax = 0;
-  if (c0 >= 0) {
-    const long long yz = (long long)a.g.ny * a.g.nz;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t < 2 * yz) {
-      const long long r = t % yz;
-      adjoint_body<L, R, CK, 0, false, true, MOM, BM, VM>(a, base, V, V, mom, t < yz ? c0 : c1,
-                                                          int(r % a.g.ny), int(r / a.g.ny), rmax);
-    }
-  } else {
-    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (x < a.g.x1)
-      adjoint_body<L, R, CK, 0, false, true, MOM, BM, VM>(a, base, V, V, mom, x, blockIdx.y,
-                                                          a.g.z0 + blockIdx.z, rmax);
-  }
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < a.g.x1)
+    adjoint_body<L, R, CK, 0, false, true, MOM, BM, VM>(a, base, V, V, mom, x, blockIdx.y,
+                                                        a.g.z0 + blockIdx.z, rmax);
 }
 
 // Side-list adjoint nodes with the full (reference-form) node update
@@ -1602,27 +1544,8 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
   }
 }
 
-template <class L, class R, int CK, bool RESID>
-__global__ void LBGPU_PAIR_BOUNDS(R) k_pair_cols(Launch a, const R* __restrict__ fsrc,
-                                                             R* __restrict__ fdst,
-                                                             const R* __restrict__ vsrc,
-                                                             R* __restrict__ vdst, int c0, int c1) {
-  const long long yz = (long long)a.g.ny * a.g.nz;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long rP = 0, rA = 0;
-  if (t < 2 * yz) {
-    const long long r = t % yz;
-    pair_body<L, R, CK, RESID>(a, fsrc, fdst, vsrc, vdst, t < yz ? c0 : c1, int(r % a.g.ny),
-                               int(r / a.g.ny), threadIdx.x, rP, rA);
-  }
-  if constexpr (RESID) {
-    detail::block_max_bits(rP, a.fl.resid);
-    detail::block_max_bits(rA, a.fl.aux);
-  }
-}
-
 // In-place fused pair (AA streaming): f from layout FM, v from layout VM,
-// each updated in place; COLS as k_primal_aa. The side-list adjoint nodes run
+// each updated in place. The side-list adjoint nodes run
 // BEFORE it (k_adjoint_side reads the base f^{n+1} that this kernel
 // overwrites; their v locations are theirs alone).
 #ifndef LBGPU_AAPAIR_MINB
@@ -1635,23 +1558,13 @@ template <class L, class R, int CK, int FM, int VM>
 __global__ void __launch_bounds__(kPairThreads<R>,
                                   (sizeof(R) == 4 ? LBGPU_AAPAIR_MINB32 : LBGPU_AAPAIR_MINB) * 128 /
                                       kPairThreads<R>)
-    k_pair_aa(Launch a, R* F, R* V, int c0, int c1) {
+    k_pair_aa(Launch a, R* F, R* V) {
   unsigned long long rP = 0, rA = 0;
-  if (c0 >= 0) {
-    const long long yz = (long long)a.g.ny * a.g.nz;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t < 2 * yz) {
-      const long long r = t % yz;
-      pair_body<L, R, CK, false, FM, VM>(a, F, F, V, V, t < yz ? c0 : c1, int(r % a.g.ny),
-                                         int(r / a.g.ny), threadIdx.x, rP, rA);
-    }
-  } else {
-    const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x < a.g.x1 && y < a.g.ny)
-      pair_body<L, R, CK, false, FM, VM>(a, F, F, V, V, x, y, a.g.z0 + blockIdx.z,
-                                         threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
-  }
+  const int x = a.g.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x < a.g.x1 && y < a.g.ny)
+    pair_body<L, R, CK, false, FM, VM>(a, F, F, V, V, x, y, a.g.z0 + blockIdx.z,
+                                       threadIdx.y * blockDim.x + threadIdx.x, rP, rA);
 }
 
 // Per-design-node gradient (param_gradient's design part, adjoint.cpp:377-398)
@@ -2230,20 +2143,20 @@ void base_moments(const Launch& a, int dim, int prec, int bm, const void* base, 
 #if defined(LBGPU_PART_AA)
 // In-place (AA) sweeps, product build: s.fm / s.vm are the current layouts
 // (FM_O / FM_E) of f and v; s.part as for the double-buffered launchers.
-// launch(a, grid, block, c0, c1): c0 >= 0 selects the boundary-column mode
+// launch(a, grid, block) for each x-range of s.part
 template <class F>
 static void aa_grid(const SweepArgs& s, F&& launch) {
   for_part(s, [&](Launch a) {
     if (a.g.x1 <= a.g.x0) return;
     const int bx = (a.g.x1 - a.g.x0) >= 128 ? 128 : ((a.g.x1 - a.g.x0) >= 64 ? 64 : 32);
-    launch(a, dim3((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz), dim3(bx), -1, -1);
+    launch(a, dim3((a.g.x1 - a.g.x0 + bx - 1) / bx, a.g.ny, a.g.nz), dim3(bx));
   });
 }
 void primal_aa(const SweepArgs& s, void* A) {
 #if !LBGPU_EXACT
   LBGPU_LR_DISPATCH(s.dim, s.prec, LBGPU_CK_DISPATCH(LBGPU_AA_DISPATCH(s.fm, FM, {
-    aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
-      k_primal_aa<L, R, CKV, FM><<<grid, block, 0, a.stream>>>(a, static_cast<R*>(A), c0, c1);
+    aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block) {
+      k_primal_aa<L, R, CKV, FM><<<grid, block, 0, a.stream>>>(a, static_cast<R*>(A));
     });
   })));
 #else
@@ -2259,16 +2172,16 @@ void adjoint_aa(const SweepArgs& s, const void* base, void* V) {
       const R* mo = static_cast<const R*>(s.mom);
       R* v = static_cast<R*>(V);
       if (mom) {  // frozen base: its moments (any base layout)
-        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
-          k_adjoint_aa<L, R, CKV, FM_O, VM, true><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block) {
+          k_adjoint_aa<L, R, CKV, FM_O, VM, true><<<grid, block, 0, a.stream>>>(a, b, v, mo);
         });
       } else if (s.fm == FM_O) {
-        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
-          k_adjoint_aa<L, R, CKV, FM_O, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block) {
+          k_adjoint_aa<L, R, CKV, FM_O, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo);
         });
       } else {
-        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block, int c0, int c1) {
-          k_adjoint_aa<L, R, CKV, FM_E, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo, c0, c1);
+        aa_grid(s, [&](const Launch& a, dim3 grid, dim3 block) {
+          k_adjoint_aa<L, R, CKV, FM_E, VM, false><<<grid, block, 0, a.stream>>>(a, b, v, mo);
         });
       }
       if (s.n_adj_side > 0 && s.part != 1) {
@@ -2314,7 +2227,7 @@ void pair_aa(const SweepArgs& s, void* F, void* V) {
         const int bx = wx >= LBGPU_AAPAIR_BX ? LBGPU_AAPAIR_BX : (wx >= 64 ? 64 : 32);
         const int by = TB / bx;
         dim3 grid((wx + bx - 1) / bx, (a.g.ny + by - 1) / by, a.g.nz);
-        k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v, -1, -1);
+        k_pair_aa<L, R, CKV, FM, VM><<<grid, dim3(bx, by), 0, a.stream>>>(a, f, v);
       });
     };
     if (s.fm == FM_O && s.vm == FM_O) go.template operator()<FM_O, FM_O>();

@@ -98,7 +98,7 @@ struct SweepArgs {
   bool resid;
   const long long* adj_side;  // adjoint side-list nodes (k_adjoint_side)
   long long n_adj_side;
-  int part;  // 0 all owned columns, 1 interior only, 2 the two boundary columns only
+  int part;  // 0 all owned columns, 2 the boundary strips only (kernels.cuh kStrip), 1 the rest
   int z0 = 0, z1 = 0;  // z planes [z0, z1) only (z1 = 0: all)
   const void* mom = nullptr;  // adjoint: cached moments of a frozen base (fast build)
   int fm = 0, vm = 0;  // addressing modes of f and v: 0 double-buffered, 1/2 in place (O/E)
