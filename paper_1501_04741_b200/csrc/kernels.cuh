@@ -155,11 +155,30 @@ __device__ __forceinline__ void gather_async_m(const R* buf, long long N, long l
   cp_async_commit();
 }
 // in-place store of node idx's post-collision values (FM_O / FM_E)
+// C3 MLUPS with / without: FP64 in-place pair 7,523 / 7,076 (its E/E form spilled 304 B
+// without), FP32 frozen-base in-place adjoint 23,103 / 18,842; the sweeps apart +0-2%.
+#ifndef LBGPU_AA_REMAT
+#define LBGPU_AA_REMAT 1
+#endif
 template <class L, class R, int D, int FM>
 __device__ __forceinline__ void store_aa(R* buf, long long N, long long idx, const Nbr& n,
                                          const R* v) {
   static_assert(FM != FM_DB, "double-buffered stores go through store_node");
-  LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, n) = v[P]; });
+  if constexpr (FM == FM_E && LBGPU_AA_REMAT) {
+    // the neighbour offsets through an opaque copy: the 26 shifted store
+    // addresses are formed here from 9 integers instead of being kept live
+    // (as the gather's) across the collision
+    Nbr m;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      asm volatile("mov.b32 %0, %1;" : "=r"(m.xs[k]) : "r"(n.xs[k]));
+      asm volatile("mov.b32 %0, %1;" : "=r"(m.ys[k]) : "r"(n.ys[k]));
+      asm volatile("mov.b32 %0, %1;" : "=r"(m.zs[k]) : "r"(n.zs[k]));
+    }
+    LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, m) = v[P]; });
+  } else {
+    LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, n) = v[P]; });
+  }
 }
 
 // Planes that cross a slab cut for a sweep pulling along D (-1 primal, +1
@@ -1024,12 +1043,13 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
 
 // In-place primal sweep (AA streaming, fast build) from layout FM over the
 // owned columns of the 3-D grid.
-// Register bound of the in-place primal (FP64): left alone, the sweep from E
-// keeps its 26 scattered store addresses live across the collision (182
-// registers, 2 blocks/SM). Measured C3 primal GB/s at 1/2/3/4 blocks per SM:
-// 5,543 / 5,535 / 5,922 / 5,648 (4: 248 B of spill).
+// Register bound of the in-place primal (FP64). Before store_aa rematerialised
+// the shifted store addresses (LBGPU_AA_REMAT) the sweep from E kept them
+// live across the collision (182 registers unbounded; C3 GB/s at 1/2/3/4
+// blocks per SM 5,543 / 5,535 / 5,922 / 5,648, 4 spilling 248 B). With it,
+// 4 blocks fit without spill: 6,408 against 6,233 at 3.
 #ifndef LBGPU_AA_PRIMAL_MINB
-#define LBGPU_AA_PRIMAL_MINB 3
+#define LBGPU_AA_PRIMAL_MINB 4
 #endif
 // FP32, 1/4/6/8 blocks per SM: 5,276 / 5,326 / 5,036 / 4,690 GB/s.
 #ifndef LBGPU_AA_PRIMAL_MINB32
@@ -1267,10 +1287,12 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
 
 // In-place adjoint sweep (AA streaming, fast build): base f read under BM, v
 // updated in place from layout VM.
-// In-place adjoint (FP64), C3 GB/s at 2/3/4 blocks per SM: 4,947 / 5,988 /
-// 5,824 (4 spills 144-472 B in the sweeps from E).
+// In-place adjoint (FP64), C3 GB/s at 2/3/4 blocks per SM without
+// LBGPU_AA_REMAT: 4,947 / 5,988 / 5,824 (4 spilled 144-472 B in the sweeps
+// from E); with it, 4 blocks: 6,487 against 6,133 at 3 (frozen base 12,335
+// against 11,185 MLUPS).
 #ifndef LBGPU_AA_ADJ_MINB
-#define LBGPU_AA_ADJ_MINB 3
+#define LBGPU_AA_ADJ_MINB 4
 #endif
 // FP32, 4/5/6/8 blocks per SM: 4,467 / 4,888 / 5,088 / 4,702 GB/s.
 #ifndef LBGPU_AA_ADJ_MINB32
