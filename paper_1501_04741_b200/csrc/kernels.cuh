@@ -1051,9 +1051,10 @@ __global__ void __launch_bounds__(128) k_primal(Launch a, const R* __restrict__ 
 #ifndef LBGPU_AA_PRIMAL_MINB
 #define LBGPU_AA_PRIMAL_MINB 4
 #endif
-// FP32, 1/4/6/8 blocks per SM: 5,276 / 5,326 / 5,036 / 4,690 GB/s.
+// FP32, blocks per SM (C3 GB/s) before LBGPU_AA_REMAT, 1/4/6/8: 5,276 / 5,326 /
+// 5,036 / 4,690; with it, 4/6/8: 5,473 / 5,646 / 5,844.
 #ifndef LBGPU_AA_PRIMAL_MINB32
-#define LBGPU_AA_PRIMAL_MINB32 4
+#define LBGPU_AA_PRIMAL_MINB32 8
 #endif
 template <class L, class R, int CK, int FM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_PRIMAL_MINB : LBGPU_AA_PRIMAL_MINB32)
@@ -1294,9 +1295,10 @@ __global__ void LBGPU_ADJ_BOUNDS(SPLIT, R, MOM) k_adjoint(Launch a,
 #ifndef LBGPU_AA_ADJ_MINB
 #define LBGPU_AA_ADJ_MINB 4
 #endif
-// FP32, 4/5/6/8 blocks per SM: 4,467 / 4,888 / 5,088 / 4,702 GB/s.
+// FP32, blocks per SM (C3 GB/s) before LBGPU_AA_REMAT, 4/5/6/8: 4,467 / 4,888 /
+// 5,088 / 4,702; with it, 6/7/8: 5,362 / 5,579 / 5,713.
 #ifndef LBGPU_AA_ADJ_MINB32
-#define LBGPU_AA_ADJ_MINB32 6
+#define LBGPU_AA_ADJ_MINB32 8
 #endif
 template <class L, class R, int CK, int BM, int VM, bool MOM>
 __global__ void __launch_bounds__(128, sizeof(R) == 8 ? LBGPU_AA_ADJ_MINB
@@ -1573,8 +1575,10 @@ __global__ void LBGPU_PAIR_BOUNDS(R) k_pair(Launch a, const R* __restrict__ fsrc
 #ifndef LBGPU_AAPAIR_MINB
 #define LBGPU_AAPAIR_MINB LBGPU_PAIR_MINB
 #endif
+// FP32 in-place pair, C3 MLUPS at 5/6/8 blocks per SM (with LBGPU_AA_REMAT):
+// 11,185 / 11,667 / 12,788.
 #ifndef LBGPU_AAPAIR_MINB32
-#define LBGPU_AAPAIR_MINB32 LBGPU_PAIR_MINB32
+#define LBGPU_AAPAIR_MINB32 8
 #endif
 template <class L, class R, int CK, int FM, int VM>
 __global__ void __launch_bounds__(kPairThreads<R>,
