@@ -90,6 +90,12 @@ __device__ __forceinline__ void gather(const R* __restrict__ buf, long long N, c
 #ifndef LBGPU_ADJ_STAGE32  // the FP32 split adjoint too
 #define LBGPU_ADJ_STAGE32 0
 #endif
+// FP32 split adjoint: v's gather addresses re-formed after the moments (opaque)
+// instead of kept from the base gather: C3 5,674 -> 5,737 GB/s (8 blocks per SM;
+// at 6 blocks 5,357).
+#ifndef LBGPU_ADJ_REMAT32
+#define LBGPU_ADJ_REMAT32 1
+#endif
 
 // Asynchronous gather into shared memory (cp.async, LDGSTS): the loads are
 // in flight without holding registers, so a sweep can issue one gather while
@@ -154,6 +160,20 @@ __device__ __forceinline__ void gather_async_m(const R* buf, long long N, long l
   LBGPU_FOR(P, 0, L::M, { cp_async_elem(smem + P * stride, in_at<L, D, FM, P>(buf, N, idx, n)); });
   cp_async_commit();
 }
+// A copy of the neighbour offsets the compiler cannot prove equal to the
+// original: addresses derived from it are recomputed where they are used
+// instead of being kept live from an earlier gather.
+__device__ __forceinline__ Nbr opaque(const Nbr& n) {
+  Nbr m;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    asm volatile("mov.b32 %0, %1;" : "=r"(m.xs[k]) : "r"(n.xs[k]));
+    asm volatile("mov.b32 %0, %1;" : "=r"(m.ys[k]) : "r"(n.ys[k]));
+    asm volatile("mov.b32 %0, %1;" : "=r"(m.zs[k]) : "r"(n.zs[k]));
+  }
+  return m;
+}
+
 // in-place store of node idx's post-collision values (FM_O / FM_E)
 // C3 MLUPS with / without: FP64 in-place pair 7,523 / 7,076 (its E/E form spilled 304 B
 // without), FP32 frozen-base in-place adjoint 23,103 / 18,842; the sweeps apart +0-2%.
@@ -165,16 +185,9 @@ __device__ __forceinline__ void store_aa(R* buf, long long N, long long idx, con
                                          const R* v) {
   static_assert(FM != FM_DB, "double-buffered stores go through store_node");
   if constexpr (FM == FM_E && LBGPU_AA_REMAT) {
-    // the neighbour offsets through an opaque copy: the 26 shifted store
-    // addresses are formed here from 9 integers instead of being kept live
-    // (as the gather's) across the collision
-    Nbr m;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      asm volatile("mov.b32 %0, %1;" : "=r"(m.xs[k]) : "r"(n.xs[k]));
-      asm volatile("mov.b32 %0, %1;" : "=r"(m.ys[k]) : "r"(n.ys[k]));
-      asm volatile("mov.b32 %0, %1;" : "=r"(m.zs[k]) : "r"(n.zs[k]));
-    }
+    // the 26 shifted store addresses formed here from 9 integers instead of
+    // being kept live (as the gather's) across the collision
+    const Nbr m = opaque(n);
     LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, m) = v[P]; });
   } else {
     LBGPU_FOR(P, 0, L::M, { *out_at<L, D, FM, P>(buf, N, idx, n) = v[P]; });
@@ -1165,6 +1178,8 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         cp_async_wait_all();
         LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
       } else if constexpr (kEarly) {
+      } else if constexpr (VM == FM_DB && LBGPU_ADJ_REMAT32) {
+        gather<L, R, +1>(src, N, opaque(nb), vin);  // offsets re-formed after the moments
       } else if constexpr (VM == FM_DB) {
         gather<L, R, +1>(src, N, nb, vin);
       } else {
