@@ -14,6 +14,8 @@
   python tools/probe.py e2e
       lbgpu_pair_step_with_design rate (with LBGPU_TRACE_PAIR=1 in the
       environment, each call's stage timeline on stderr)
+  python tools/probe.py e2e_alt
+      the same call alternating with and without J, each call timed (the cost of J)
   python tools/probe.py l2gran
       objective / pair / e2e rates under each cudaLimitMaxL2FetchGranularity
   python tools/probe.py ncu {pair,sweeps,gradient,aa,e2e,sweeps32}
