@@ -87,6 +87,18 @@ __device__ __forceinline__ void gather(const R* __restrict__ buf, long long N, c
 #ifndef LBGPU_ADJ_STAGE
 #define LBGPU_ADJ_STAGE 1
 #endif
+// FP64 split adjoint: the VJP reads the staged v in place instead of from a
+// register copy. C3 with / without: frozen base 12,831 / 12,569 MLUPS, in
+// place 6,582 / 6,497 GB/s (frozen 12,559 / 12,114); at 5 blocks per SM it
+// spills 96 B and is slower.
+#ifndef LBGPU_ADJ_VSMEM
+#define LBGPU_ADJ_VSMEM 1
+#endif
+// Fused pair: its adjoint half reading the staged v in place measured no
+// different (C3 7,699 against 7,692-7,695 MLUPS): off.
+#ifndef LBGPU_PAIR_VSMEM
+#define LBGPU_PAIR_VSMEM 0
+#endif
 #ifndef LBGPU_ADJ_STAGE32  // the FP32 split adjoint too
 #define LBGPU_ADJ_STAGE32 0
 #endif
@@ -408,20 +420,10 @@ __device__ __forceinline__ void flow_sums(const R* f, R& rho, R* j) {
 
 // The interior VJP reads the base state only through rho, u and T
 // (adjoint.cpp:59, :95): the moment-form entry point takes those.
-template <class L, class R, int CK>
-__device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double omt, R rho,
-                                            R inv, const R* jv, R T, const R* vf, const R* vg,
-                                            R* outf, R* outg);
-template <class L, class R, int CK>
-__device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double omt, R rho,
-                                           const R* jv, R T, const R* vf, const R* vg, R* outf,
-                                           R* outg) {
-  if (!(rho > R(0))) return false;
-  fast_vjp_mi<L, R, CK>(M, pp, omt, rho, R(1) / rho, jv, T, vf, vg, outf, outg);
-  return true;
-}
+// VS: the stride of vf / vg (1: registers; 128: a thread's slots of a
+// shared-memory staging buffer, read in place).
 // The VJP given 1/rho (rho > 0 checked by the caller).
-template <class L, class R, int CK>
+template <class L, class R, int CK, int VS = 1>
 __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double omt, R rho,
                                             R inv, const R* jv, R T, const R* vf, const R* vg,
                                             R* outf, R* outg) {
@@ -441,7 +443,7 @@ __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double o
         R m = R(0);
         LBGPU_FOR(J, 0, L::MF, {
           constexpr double uij = L::U(I, J);
-          if constexpr (uij != 0.0) m += R(uij) * vf[J];
+          if constexpr (uij != 0.0) m += R(uij) * vf[J * VS];
         });
         mm[I] = m * R(M.mrt_c[I]);
       }
@@ -450,7 +452,7 @@ __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double o
   const R cb = R(1.0 - M.om);
   auto rj = [&]<int J>() -> R {
     if constexpr (CK == 0) {
-      return cb * vf[J];
+      return cb * vf[J * VS];
     } else {
       R acc = R(0);
       LBGPU_FOR(I, 0, L::MF, {
@@ -467,7 +469,7 @@ __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double o
   R Pu[3] = {R(0), R(0), R(0)}, Ru[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MF, {
     const R eu = edotp<L, R, J>(u), eup = edotp<L, R, J>(up);
-    const R tv = R(L::wf(J)) * vf[J];
+    const R tv = R(L::wf(J)) * vf[J * VS];
     const R tr = R(L::wf(J)) * rj.template operator()<J>();
     Pr += tv * (b0 + eup * (R(3) + R(4.5) * eup));
     Rr += tr * (a0 + eu * (R(3) + R(4.5) * eu));
@@ -487,7 +489,7 @@ __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double o
 
   R St0 = R(0), St1[3] = {R(0), R(0), R(0)};
   LBGPU_FOR(J, 0, L::MT, {
-    const R tw = R(L::wt(J)) * vg[J];
+    const R tw = R(L::wt(J)) * vg[J * VS];
     St0 += tw;
     if constexpr (L::et(J, 0) != 0) St1[0] += L::et(J, 0) > 0 ? tw : -tw;
     if constexpr (L::et(J, 1) != 0) St1[1] += L::et(J, 1) > 0 ? tw : -tw;
@@ -504,7 +506,15 @@ __device__ __forceinline__ void fast_vjp_mi(const Model& M, PowPair pp, double o
   LBGPU_FOR(K_, 0, L::MF, { outf[K_] = rj.template operator()<K_>() + s0 + edotp<L, R, K_>(ci); });
   const R om1 = R(1) - om, oms = om * sigma;
 #pragma unroll
-  for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k] + oms;
+  for (int k = 0; k < L::MT; ++k) outg[k] = om1 * vg[k * VS] + oms;
+}
+template <class L, class R, int CK, int VS = 1>
+__device__ __forceinline__ bool fast_vjp_m(const Model& M, PowPair pp, double omt, R rho,
+                                           const R* jv, R T, const R* vf, const R* vg, R* outf,
+                                           R* outg) {
+  if (!(rho > R(0))) return false;
+  fast_vjp_mi<L, R, CK, VS>(M, pp, omt, rho, R(1) / rho, jv, T, vf, vg, outf, outg);
+  return true;
 }
 
 template <class L, class R, int CK>
@@ -1098,6 +1108,8 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
                                              const R* src, R* dst, const R* __restrict__ mom,
                                              int x, int y, int z, unsigned long long& rmax) {
   using namespace detail;
+  constexpr bool kInSmem = !LBGPU_EXACT && AK == 0 && SPLIT && LBGPU_ADJ_STAGE && sizeof(R) == 8 &&
+                           LBGPU_ADJ_VSMEM;
   const Geom& g = a.g;
   const long long N = g.N;
   const long long idx = x + (long long)g.nx * (y + (long long)g.ny * z);
@@ -1174,9 +1186,12 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
           }
         }
       }
+      // kInSmem: the staged v is read in place by the VJP (no register copy)
+      constexpr int VS = kInSmem ? 128 : 1;
+      const R* vv = kInSmem ? my : vin;
       if constexpr (kStage) {
         cp_async_wait_all();
-        LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
+        if constexpr (!kInSmem) LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * 128]; });
       } else if constexpr (kEarly) {
       } else if constexpr (VM == FM_DB && LBGPU_ADJ_REMAT32) {
         gather<L, R, +1>(src, N, opaque(nb), vin);  // offsets re-formed after the moments
@@ -1186,17 +1201,17 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
         gather_m<L, R, +1, VM>(src, N, idx, nb, vin);
       }
       if (tag == TAG_WALL) {
-        LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+        LBGPU_FOR(P, 0, L::M, { vout[P] = vv[copp<L>(P) * VS]; });
       } else if (tag == TAG_HEATER) {
-        LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+        LBGPU_FOR(P, 0, L::MF, { vout[P] = vv[L::oppf(P) * VS]; });
 #pragma unroll
         for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
       } else {
         const double w = (code & CODE_HAS_W) ? a.t.w[idx] : 1.0;
         const PowPair pp = node_pp<false>(a.M, a.t, idx, code, w);
         const double omt = node_omt<R>(a.M, a.t, code, w);
-        ok = fast_vjp_m<L, R, CK>(a.M, pp, omt, rho, jv, T, vin, vin + L::MF, vout,
-                                  vout + L::MF);
+        ok = fast_vjp_m<L, R, CK, VS>(a.M, pp, omt, rho, jv, T, vv, vv + L::MF * VS, vout,
+                                      vout + L::MF);
         if (face) {
           const bool inlet = tag == TAG_INLET;
           face_dispatch<L>(code, [&]<int AX, int SG>() {
@@ -1208,7 +1223,7 @@ __device__ __forceinline__ void adjoint_body(const Launch& a, const R* __restric
     }
     if (!ok) atomicMin(a.fl.bad, (a.fl.step_key | (unsigned long long)gflat(g, x, y, z)));
     if constexpr (VM == FM_DB) {
-      store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax);
+      store_node<L, R, RESID>(src, dst, N, idx, vin, vout, rmax, !kInSmem);
       push_halo<L, R, +1>(a, x, y, z, vout);
     } else {
       static_assert(!RESID, "in-place sweeps keep no old state for the residual");
@@ -1504,18 +1519,22 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
   }
   if (!side) {
     R vin[L::M], vout[L::M];
+    // kInSmem: the VJP reads the staged v in place (no register copy)
+    constexpr bool kInSmem = kStage && LBGPU_PAIR_VSMEM;
+    constexpr int VS = kInSmem ? kTB : 1;
+    const R* vv = kInSmem ? my : vin;
     if constexpr (kStage) {
       cp_async_wait_all();
-      LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * kTB]; });
+      if constexpr (!kInSmem) LBGPU_FOR(P, 0, L::M, { vin[P] = my[P * kTB]; });
     } else if constexpr (VM == FM_DB) {
       gather<L, R, +1>(vsrc, N, nb, vin);
     } else {
       gather_m<L, R, +1, VM>(vsrc, N, idx, nb, vin);
     }
     if (tag == TAG_WALL) {
-      LBGPU_FOR(P, 0, L::M, { vout[P] = vin[copp<L>(P)]; });
+      LBGPU_FOR(P, 0, L::M, { vout[P] = vv[copp<L>(P) * VS]; });
     } else if (tag == TAG_HEATER) {
-      LBGPU_FOR(P, 0, L::MF, { vout[P] = vin[L::oppf(P)]; });
+      LBGPU_FOR(P, 0, L::MF, { vout[P] = vv[L::oppf(P) * VS]; });
 #pragma unroll
       for (int j = 0; j < L::MT; ++j) vout[L::MF + j] = R(0);
     } else {
@@ -1529,7 +1548,7 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
         }
       }
       if (rho > R(0))
-        fast_vjp_mi<L, R, CK>(a.M, ppa, omta, rho, inv, jv, T, vin, vin + L::MF, vout, vout + L::MF);
+        fast_vjp_mi<L, R, CK, VS>(a.M, ppa, omta, rho, inv, jv, T, vv, vv + L::MF * VS, vout, vout + L::MF);
       else
         okA = false;
       if (face) {
@@ -1541,7 +1560,7 @@ __device__ __forceinline__ void pair_body(const Launch& a, const R* fsrc, R* fds
     }
     if (a.M.obj_on && (code & CODE_SUPPORT)) okA = fast_partial_m<L, R>(a.M, rho, jv, T, vout) && okA;
     if constexpr (VM == FM_DB) {
-      store_node<L, R, RESID>(vsrc, vdst, N, idx, vin, vout, rA);
+      store_node<L, R, RESID>(vsrc, vdst, N, idx, vin, vout, rA, !kInSmem);
       push_halo<L, R, +1>(a, x, y, z, vout);
     } else {
       store_aa<L, R, +1, VM>(vdst, N, idx, nb, vout);
